@@ -1,0 +1,482 @@
+// extern "C" boundary (include/feinsum_b200.h). Every entry point converts
+// exceptions into status codes + a thread-local message, so no C++ exception
+// ever crosses the ABI.
+#include "feinsum_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <string>
+
+#include "feinsum/canonicalize.hpp"
+#include "feinsum/factsdb.hpp"
+#include "feinsum/induced_graph.hpp"
+#include "feinsum/notation.hpp"
+#include "feinsum/raising.hpp"
+#include "json.hpp"
+#include "planner.hpp"
+#include "einsum_json.hpp"  // after the feinsum headers
+
+using fejson::Value;
+using namespace feinsum;
+
+struct fe_plan_s {
+  std::unique_ptr<feb200::Plan> plan;
+  // staging buffers for fe_plan_execute_host, allocated on first use
+  std::vector<void*> staged_in, staged_out;
+  ~fe_plan_s() {
+    for (void* p : staged_in) cudaFree(p);
+    for (void* p : staged_out) cudaFree(p);
+  }
+};
+
+namespace {
+
+thread_local std::string g_last;
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+int guarded(const std::function<void()>& f) {
+  try {
+    f();
+    return FE_OK;
+  } catch (const feinsum::error& e) {
+    g_last = e.what();
+    return 1 + static_cast<int>(e.kind());
+  } catch (const std::bad_alloc&) {
+    g_last = "out of host memory";
+    return FE_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last = e.what();
+    return FE_ERR_INTERNAL;
+  }
+}
+
+int cuda_status(int e) {
+  if (e == 0) return FE_OK;
+  g_last = std::string("CUDA error: ") + cudaGetErrorString(static_cast<cudaError_t>(e));
+  return FE_ERR_CUDA;
+}
+
+BatchedEinsum ein(const char* js) { return transport::einsum_from_json(fejson::parse(js)); }
+void put(char** out, const Value& v) { *out = dup(fejson::dump(v)); }
+
+Value graph_json(const ColoredDigraph& g) {
+  Value v = Value::obj();
+  v.set("n", Value::num(g.n));
+  Value colors = Value::arr();
+  for (int c : g.colors) colors.push(Value::num(c));
+  v.set("colors", std::move(colors));
+  Value edges = Value::arr();
+  for (int i = 0; i < g.n; ++i)
+    for (int j = 0; j < g.n; ++j)
+      if (g.edge(i, j)) {
+        Value e = Value::arr();
+        e.push(Value::num(i));
+        e.push(Value::num(j));
+        edges.push(std::move(e));
+      }
+  v.set("edges", std::move(edges));
+  return v;
+}
+
+ColoredDigraph graph_from(const Value& v) {
+  ColoredDigraph g = ColoredDigraph::empty(static_cast<int>(v.at("n").as_int()));
+  size_t k = 0;
+  for (const auto& c : v.at("colors").a) g.colors.at(k++) = static_cast<int>(c.as_int());
+  for (const auto& e : v.at("edges").a) g.set_edge(static_cast<int>(e.a[0].as_int()), static_cast<int>(e.a[1].as_int()));
+  return g;
+}
+
+Expr expr_from(const Value& v) {
+  Expr e;
+  if (auto* x = v.find("lit")) {
+    e.kind = Expr::Kind::literal;
+    e.literal = x->as_double();
+  } else if (auto* x = v.find("param")) {
+    e.kind = Expr::Kind::param;
+    e.name = x->as_str();
+  } else if (auto* x = v.find("read")) {
+    e.kind = Expr::Kind::access;
+    e.name = x->as_str();
+    e.subs = transport::list_from_json(v.at("subs"));
+  } else if (auto* x = v.find("fn")) {
+    e.kind = Expr::Kind::unary;
+    e.name = x->as_str();
+    e.children.push_back(expr_from(v.at("x")));
+  } else if (auto* x = v.find("op")) {
+    e.kind = Expr::Kind::binary;
+    e.op = x->as_str().at(0);
+    e.children.push_back(expr_from(v.at("l")));
+    e.children.push_back(expr_from(v.at("r")));
+  } else {
+    throw error(errc::usage, "expression node needs one of lit/param/read/fn/op");
+  }
+  return e;
+}
+
+Value canon_json(const CanonResult& c) {
+  Value v = Value::obj();
+  v.set("canonical", transport::einsum_to_json(c.canonical));
+  v.set("sigma_idx", transport::strmap_to_json(c.sigma_idx));
+  v.set("sigma_arg", transport::strmap_to_json(c.sigma_arg));
+  v.set("sigma_row", transport::ints_to_json(c.sigma_row));
+  v.set("sigma_slot", transport::ints_to_json(c.sigma_slot));
+  return v;
+}
+
+}  // namespace
+
+namespace feinsum::detail {
+std::string key_of_canonical(const BatchedEinsum& e);
+}
+
+extern "C" {
+
+const char* fe_last_error(void) { return g_last.c_str(); }
+void fe_free(void* p) { std::free(p); }
+int fe_version(void) { return 1; }
+
+int fe_device_check(void) {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    g_last = std::string("no usable CUDA device (") + cudaGetErrorString(e) + ")";
+    return FE_ERR_IO;
+  }
+  return FE_OK;
+}
+
+int fe_parse_classic(const char* text, char** out) {
+  return guarded([&] { put(out, transport::einsum_to_json(parse_classic(text))); });
+}
+
+int fe_print_classic(const char* js, char** out) {
+  return guarded([&] { *out = dup(print_classic(ein(js))); });
+}
+
+int fe_validate(const char* js, char** out) {
+  return guarded([&] { put(out, transport::list_to_json(validate(ein(js)))); });
+}
+
+int fe_canonicalize(const char* js, char** out) {
+  return guarded([&] {
+    const CanonResult c = canonicalize(ein(js));
+    Value v = canon_json(c);
+    v.set("key", Value::str(feinsum::detail::key_of_canonical(c.canonical)));
+    put(out, v);
+  });
+}
+
+int fe_canonical_key(const char* js, char** out) {
+  return guarded([&] { *out = dup(canonical_key(ein(js))); });
+}
+
+int fe_is_isomorphic(const char* a, const char* b, char** out) {
+  return guarded([&] {
+    const auto w = is_isomorphic(ein(a), ein(b));
+    put(out, w ? transport::witness_to_json(*w) : Value{});
+  });
+}
+
+int fe_brute_force_isomorphic(const char* a, const char* b, uint64_t budget, char** out) {
+  return guarded([&] {
+    const auto w = brute_force_isomorphic(ein(a), ein(b), budget);
+    put(out, w ? transport::witness_to_json(*w) : Value{});
+  });
+}
+
+int fe_verify_witness(const char* a, const char* b, const char* w, char** out) {
+  return guarded([&] {
+    std::vector<std::string> why;
+    const bool ok =
+        verify_witness(ein(a), ein(b), transport::witness_from_json<SubstitutionWitness>(fejson::parse(w)), &why);
+    Value v = Value::obj();
+    v.set("ok", Value::boolean_(ok));
+    v.set("why", transport::list_to_json(why));
+    put(out, v);
+  });
+}
+
+int fe_generate_random(const char* params_js, uint64_t seed, char** out) {
+  return guarded([&] {
+    GenParams p;
+    const Value pv = fejson::parse(params_js);
+    auto geti = [&](const char* k, int& dst) {
+      if (auto* x = pv.find(k)) dst = static_cast<int>(x->as_int());
+    };
+    geti("b_min", p.b_min);
+    geti("b_max", p.b_max);
+    geti("n_min", p.n_min);
+    geti("n_max", p.n_max);
+    geti("max_indices", p.max_indices);
+    geti("max_dim", p.max_dim);
+    if (auto* x = pv.find("shape_pool")) {
+      p.shape_pool.clear();
+      for (const auto& s : x->a) p.shape_pool.push_back(s.as_int());
+    }
+    if (auto* x = pv.find("dtype_pool")) {
+      p.dtype_pool.clear();
+      for (const auto& s : x->a) p.dtype_pool.push_back(dtype_from_name(s.as_str()));
+    }
+    if (auto* x = pv.find("allow_empty_out")) p.allow_empty_out = x->b;
+    if (auto* x = pv.find("allow_repeated_index")) p.allow_repeated_index = x->b;
+    put(out, transport::einsum_to_json(generate_random(p, seed)));
+  });
+}
+
+int fe_scramble(const char* js, uint64_t seed, char** out) {
+  return guarded([&] {
+    const Scrambled s = scramble(ein(js), seed);
+    Value v = Value::obj();
+    v.set("e", transport::einsum_to_json(s.e));
+    v.set("w", transport::witness_to_json(s.w));
+    put(out, v);
+  });
+}
+
+int fe_induced_graph(const char* js, int64_t shuffle_seed, char** out) {
+  return guarded([&] {
+    std::optional<std::uint64_t> seed;
+    if (shuffle_seed >= 0) seed = static_cast<std::uint64_t>(shuffle_seed);
+    const InducedGraph ig = to_induced_graph(ein(js), seed);
+    Value v = graph_json(ig.graph);
+    Value ia = Value::obj(), ii = Value::obj(), io = Value::obj(), ip = Value::obj(), il = Value::obj(),
+          idt = Value::obj();
+    for (const auto& [k, x] : ig.iota_arg) ia.set(std::to_string(k), Value::str(x));
+    for (const auto& [k, x] : ig.iota_index) ii.set(std::to_string(k), Value::str(x));
+    for (const auto& [k, x] : ig.iota_output) io.set(std::to_string(k), Value::num(x));
+    for (const auto& [k, x] : ig.iota_argpos) ip.set(std::to_string(k), Value::num(x));
+    for (const auto& [k, x] : ig.iota_length) il.set(std::to_string(k), Value::num(x));
+    for (const auto& [k, x] : ig.iota_dtype) idt.set(std::to_string(k), Value::str(dtype_name(x)));
+    v.set("iota_arg", std::move(ia));
+    v.set("iota_index", std::move(ii));
+    v.set("iota_output", std::move(io));
+    v.set("iota_argpos", std::move(ip));
+    v.set("iota_length", std::move(il));
+    v.set("iota_dtype", std::move(idt));
+    put(out, v);
+  });
+}
+
+int fe_canonical_labeling(const char* graph_js, char** out) {
+  return guarded([&] { put(out, transport::ints_to_json(canonical_labeling(graph_from(fejson::parse(graph_js))).perm)); });
+}
+
+int fe_check_compliance(const char* graph_js, char** out) {
+  return guarded([&] { put(out, transport::list_to_json(check_compliance(graph_from(fejson::parse(graph_js))))); });
+}
+
+int fe_raise(const char* fk, char** out) {
+  return guarded([&] {
+    const FunctionalKernel k = parse_kernel(fk);
+    const RaiseResult rr = raise_to_batched_einsum(k);
+    Value v = Value::obj();
+    v.set("skeleton", transport::einsum_to_json(rr.f.skeleton));
+    v.set("sigma_arg", transport::strmap_to_json(rr.sigma_arg));
+    v.set("sigma_idx", transport::strmap_to_json(rr.sigma_idx));
+    Value fps = Value::obj();
+    for (const auto& [name, op] : rr.f.operand_map) fps.set(name, Value::str(fingerprint(op)));
+    v.set("fingerprints", std::move(fps));
+    v.set("idealized", Value::boolean_(is_idealized(rr.f)));
+    v.set("printed", Value::str(print_kernel(k)));
+    put(out, v);
+  });
+}
+
+int fe_identify(const char* fk, const char* js, char** out) {
+  return guarded([&] {
+    const MatchResult m = identify_as_einsum(parse_kernel(fk), ein(js));
+    Value v = Value::obj();
+    v.set("sigma_idx", transport::strmap_to_json(m.sigma_idx));
+    v.set("sigma_arg", transport::strmap_to_json(m.sigma_arg));
+    v.set("sigma_arg_skeleton", transport::strmap_to_json(m.sigma_arg_skeleton));
+    v.set("sigma_row", transport::ints_to_json(m.sigma_row));
+    put(out, v);
+  });
+}
+
+int fe_cost(const char* js, char** out) {
+  return guarded([&] {
+    const BatchedEinsum e = ein(js);
+    Value v = Value::obj();
+    v.set("flop_count", Value::dbl(flop_count(e)));
+    v.set("footprint_bytes", Value::dbl(footprint_bytes(e)));
+    v.set("arithmetic_intensity", Value::dbl(arithmetic_intensity(e)));
+    v.set("algorithmic_flops", Value::dbl(feb200::optimal_path_flops(e) * e.b()));
+    Value presets = Value::obj();
+    for (const DeviceModel& d : device_presets()) {
+      Value p = Value::obj();
+      p.set("roofline_flop_rate", Value::dbl(roofline_flop_rate(e, d)));
+      p.set("memory_bound", Value::boolean_(memory_bound(e, d)));
+      presets.set(d.id, std::move(p));
+    }
+    v.set("presets", std::move(presets));
+    put(out, v);
+  });
+}
+
+int fe_record_facts(const char* path, const char* facts_js) {
+  return guarded([&] {
+    std::vector<FactRecord> batch;
+    for (const auto& f : fejson::parse(facts_js).a) {
+      FactRecord r;
+      r.canonical_key = f.at("canonical_key").as_str();
+      r.device_id = f.at("device_id").as_str();
+      r.transform_id = f.at("transform_id").as_str();
+      r.wall_time_s = f.at("wall_time_s").as_double();
+      r.flop_rate = f.at("flop_rate").as_double();
+      if (auto* x = f.find("recorded_at")) r.recorded_at = x->as_str();
+      if (auto* x = f.find("meta")) r.meta = x->as_str();
+      batch.push_back(std::move(r));
+    }
+    record_facts(path, batch);
+  });
+}
+
+int fe_retrieve(const char* path, const char* key, const char* device, char** out) {
+  return guarded([&] {
+    const auto r = retrieve(path, key, device);
+    if (!r) {
+      put(out, Value{});
+      return;
+    }
+    Value v = Value::obj();
+    v.set("canonical_key", Value::str(r->canonical_key));
+    v.set("device_id", Value::str(r->device_id));
+    v.set("transform_id", Value::str(r->transform_id));
+    v.set("wall_time_s", Value::dbl(r->wall_time_s));
+    v.set("flop_rate", Value::dbl(r->flop_rate));
+    v.set("recorded_at", Value::str(r->recorded_at));
+    v.set("meta", Value::str(r->meta));
+    put(out, v);
+  });
+}
+
+// ------------------------------------------------------------------ plans --
+
+int fe_plan_create(const char* js, const char* options, fe_plan_t* out) {
+  return guarded([&] {
+    auto h = std::make_unique<fe_plan_s>();
+    h->plan = feb200::make_plan(ein(js), feb200::parse_options(options ? options : ""));
+    *out = h.release();
+  });
+}
+
+int fe_plan_create_kernel(const char* fk, const char* options, fe_plan_t* out) {
+  return guarded([&] {
+    const FunctionalKernel k = parse_kernel(fk);
+    const RaiseResult rr = raise_to_batched_einsum(k);
+    auto h = std::make_unique<fe_plan_s>();
+    h->plan = feb200::make_functional_plan(rr.f.skeleton, rr.f.operand_map, k.arrays,
+                                           feb200::parse_options(options ? options : ""));
+    *out = h.release();
+  });
+}
+
+int fe_plan_create_functional(const char* js, const char* options, fe_plan_t* out) {
+  return guarded([&] {
+    const Value v = fejson::parse(js);
+    const BatchedEinsum skel = transport::einsum_from_json(v.at("skeleton"));
+    std::map<std::string, OperandExpr> ops;
+    for (const auto& [name, o] : v.at("operands").o)
+      ops[name] = OperandExpr{transport::list_from_json(o.at("params")), expr_from(o.at("body"))};
+    std::map<std::string, ArrayMeta> arrays;
+    for (const auto& m : v.at("arrays").a) {
+      ArrayMeta meta = transport::meta_from_json(m);
+      arrays[meta.name] = meta;
+    }
+    auto h = std::make_unique<fe_plan_s>();
+    h->plan = feb200::make_functional_plan(skel, ops, arrays, feb200::parse_options(options ? options : ""));
+    *out = h.release();
+  });
+}
+
+int fe_plan_describe(fe_plan_t plan, char** out) {
+  return guarded([&] { *out = dup(feb200::describe(*plan->plan)); });
+}
+
+int fe_plan_num_inputs(fe_plan_t plan) { return static_cast<int>(plan->plan->leaves.size()); }
+int fe_plan_num_outputs(fe_plan_t plan) { return static_cast<int>(plan->plan->outputs.size()); }
+
+int fe_plan_execute(fe_plan_t plan, const void* const* d_in, void* const* d_out, void* stream) {
+  return guarded([&] {
+    if (!plan->plan->d_blob) throw error(errc::usage, "plan was created with dry_run; it cannot execute");
+    feb200::execute(*plan->plan, d_in, d_out, stream);
+  });
+}
+
+int fe_plan_execute_host(fe_plan_t plan, const void* const* h_in, void* const* h_out, void* stream) {
+  return guarded([&] {
+    const feb200::Plan& p = *plan->plan;
+    auto ensure = [](std::vector<void*>& bufs, size_t i, std::int64_t bytes) {
+      if (bufs.size() <= i) bufs.resize(i + 1, nullptr);
+      if (!bufs[i]) {
+        const cudaError_t e = cudaMalloc(&bufs[i], static_cast<size_t>(bytes > 0 ? bytes : 16));
+        if (e != cudaSuccess) throw error(errc::io, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+      }
+      return bufs[i];
+    };
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<const void*> din;
+    for (size_t i = 0; i < p.leaves.size(); ++i) {
+      void* d = ensure(plan->staged_in, i, p.leaves[i].bytes());
+      const cudaError_t e = cudaMemcpyAsync(d, h_in[i], static_cast<size_t>(p.leaves[i].bytes()),
+                                            cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) throw error(errc::io, std::string("H2D: ") + cudaGetErrorString(e));
+      din.push_back(d);
+    }
+    std::vector<void*> dout;
+    for (size_t r = 0; r < p.outputs.size(); ++r) dout.push_back(ensure(plan->staged_out, r, p.outputs[r].bytes()));
+    feb200::execute(p, din.data(), dout.data(), stream);
+    for (size_t r = 0; r < p.outputs.size(); ++r) {
+      const cudaError_t e = cudaMemcpyAsync(h_out[r], dout[r], static_cast<size_t>(p.outputs[r].bytes()),
+                                            cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) throw error(errc::io, std::string("D2H: ") + cudaGetErrorString(e));
+    }
+  });
+}
+
+int fe_plan_tabulate(fe_plan_t plan, const char* operand, const void* const* d_in, double* d_out, int64_t first,
+                     int64_t count, void* stream) {
+  return guarded([&] { feb200::tabulate(*plan->plan, operand, d_in, d_out, first, count, stream); });
+}
+
+int fe_plan_shard(fe_plan_t plan, int rank, int world, const char* options, fe_plan_t* out, int64_t* lo, int64_t* hi,
+                  char** axis) {
+  return guarded([&] {
+    std::string ax;
+    auto h = std::make_unique<fe_plan_s>();
+    h->plan = feb200::make_shard(*plan->plan, rank, world, feb200::parse_options(options ? options : ""), lo, hi, &ax);
+    *axis = dup(ax);
+    *out = h.release();
+  });
+}
+
+int fe_plan_destroy(fe_plan_t plan) {
+  delete plan;
+  return FE_OK;
+}
+
+int fe_fill_dyadic(void* d_ptr, int storage, int64_t count, uint64_t seed, void* stream) {
+  return cuda_status(feb200::fill_dyadic(d_ptr, storage, count, seed, stream));
+}
+
+int fe_flush_l2(void* d_scratch, int64_t bytes, void* stream) {
+  return cuda_status(feb200::flush_l2(d_scratch, bytes, stream));
+}
+
+int fe_sm_count(void) {
+  int n = 0;
+  if (feb200::device_sm_count(&n) != 0) return -1;
+  return n;
+}
+
+}  // extern "C"

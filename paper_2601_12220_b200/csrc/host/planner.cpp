@@ -1,0 +1,1034 @@
+// B200 planner — see planner.hpp for the pipeline. Canonicalization drives
+// dispatch exactly as the paper intends: the tuned choice is stored per normal
+// form (canonical key -> fact), the kernel family is matched on the canonical
+// form, and the sigma maps (canonical -> caller) route the caller's buffers to
+// the kernel's roles. Since canonical slot j has the same layout as caller slot
+// sigma_slot[j], no data is ever transposed.
+#include "planner.hpp"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <numeric>
+#include <set>
+#include <sstream>
+
+#include "feinsum/notation.hpp"
+#include "json.hpp"
+#include "einsum_json.hpp"  // after the feinsum headers
+
+namespace feinsum::detail {
+std::string key_of_canonical(const BatchedEinsum& e);
+}
+
+namespace feb200 {
+
+using feinsum::errc;
+using feinsum::error;
+using feinsum::Expr;
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw error(errc::io, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+void cuda_check(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
+
+}  // namespace
+
+const char* family_transform(Family f) {
+  switch (f) {
+    case Family::generic: return "generic/v1";
+    case Family::fem_grad: return "fem_grad/v1";
+    case Family::gett: return "gett_dmma/v1";
+    case Family::tt: return "tt/v1";
+    case Family::hex: return "hex_sumfact/v1";
+  }
+  return "generic/v1";
+}
+
+int storage_from_name(const std::string& s) {
+  static const std::map<std::string, int> m = {{"f64", ST_F64}, {"f32", ST_F32}, {"c128", ST_C128}, {"c64", ST_C64},
+                                               {"i8", ST_I8},   {"i32", ST_I32}, {"i64", ST_I64},   {"f16", ST_F16}};
+  auto it = m.find(s);
+  if (it == m.end()) throw error(errc::usage, "unknown storage \"" + s + "\"");
+  return it->second;
+}
+
+const char* storage_name(int st) {
+  static const char* names[] = {"f64", "f32", "c128", "c64", "i8", "i32", "i64", "f16"};
+  return (st >= 0 && st < 8) ? names[st] : "?";
+}
+
+int native_storage(Dtype t) {
+  switch (t) {
+    case Dtype::int8: return ST_I8;
+    case Dtype::int32: return ST_I32;
+    case Dtype::int64: return ST_I64;
+    case Dtype::float16: return ST_F16;
+    case Dtype::float32: return ST_F32;
+    case Dtype::float64: return ST_F64;
+    case Dtype::complex64: return ST_C64;
+    case Dtype::complex128: return ST_C128;
+  }
+  return ST_F64;
+}
+
+namespace {
+bool is_complex_dtype(Dtype t) { return t == Dtype::complex64 || t == Dtype::complex128; }
+}  // namespace
+
+std::string default_facts_path() {
+  Dl_info info{};
+  if (dladdr(reinterpret_cast<void*>(&default_facts_path), &info) && info.dli_fname) {
+    std::string so = info.dli_fname;
+    const auto slash = so.rfind('/');
+    const std::string dir = slash == std::string::npos ? "." : so.substr(0, slash);
+    return dir + "/../facts/b200.facts";
+  }
+  return "paper_2601_12220_b200/facts/b200.facts";
+}
+
+PlanOptions parse_options(const std::string& json) {
+  PlanOptions o;
+  if (json.empty()) return o;
+  const fejson::Value v = fejson::parse(json);
+  if (v.t != fejson::Value::T::object) throw error(errc::usage, "options must be a JSON object");
+  if (auto* x = v.find("storage")) {
+    if (x->t == fejson::Value::T::string) {
+      o.storage = x->s;
+      if (o.storage != "native" && o.storage != "wide")
+        throw error(errc::usage, "options.storage must be \"native\" or \"wide\"");
+    } else {
+      for (const auto& [name, st] : x->o) o.storage_of[name] = st.as_str();
+    }
+  }
+  if (auto* x = v.find("facts")) o.facts_path = x->as_str();
+  if (auto* x = v.find("device")) o.device_id = x->as_str();
+  if (auto* x = v.find("transform")) o.force_transform = x->as_str();
+  if (auto* x = v.find("canonicalize")) o.canonicalize = x->b;
+  if (auto* x = v.find("dry_run")) o.dry_run = x->b;
+  return o;
+}
+
+// ------------------------------------------------------------- facts index --
+
+namespace {
+
+// In-process index over a facts file: retrieve() semantics (least wall time,
+// ties to newest recorded_at, then later row), loaded once per path/mtime.
+class FactsIndex {
+ public:
+  std::optional<feinsum::FactRecord> best(const std::string& path, const std::string& key,
+                                          const std::string& device) {
+    std::lock_guard<std::mutex> lock(mu_);
+    auto& entry = cache_[path];
+    if (!entry.loaded) {
+      entry.loaded = true;
+      try {
+        for (auto& r : feinsum::load_facts(path)) {
+          auto& slot = entry.best[r.canonical_key + "\x1f" + r.device_id];
+          const bool better = !slot || r.wall_time_s < slot->wall_time_s ||
+                              (r.wall_time_s == slot->wall_time_s && r.recorded_at >= slot->recorded_at);
+          if (better) slot = r;
+        }
+      } catch (const error&) {
+        entry.best.clear();
+      }
+    }
+    auto it = entry.best.find(key + "\x1f" + device);
+    if (it == entry.best.end()) return std::nullopt;
+    return it->second;
+  }
+  void invalidate() {
+    std::lock_guard<std::mutex> lock(mu_);
+    cache_.clear();
+  }
+
+ private:
+  struct Entry {
+    bool loaded = false;
+    std::map<std::string, std::optional<feinsum::FactRecord>> best;
+  };
+  std::mutex mu_;
+  std::map<std::string, Entry> cache_;
+};
+
+FactsIndex& facts_index() {
+  static FactsIndex idx;
+  return idx;
+}
+
+// ------------------------------------------------------ operand compilation --
+
+void flatten_chain(const Expr& e, char a, char b, std::vector<std::pair<char, const Expr*>>& out) {
+  // left-deep chain of a/b operators: ((t0 op t1) op t2) ...
+  if (e.kind == Expr::Kind::binary && (e.op == a || e.op == b)) {
+    flatten_chain(e.children[0], a, b, out);
+    out.emplace_back(e.op, &e.children[1]);
+    return;
+  }
+  out.emplace_back(0, &e);
+}
+
+bool uses_sqrt(const Expr& e) {
+  if (e.kind == Expr::Kind::unary && e.name == "sqrt") return true;
+  for (const Expr& c : e.children)
+    if (uses_sqrt(c)) return true;
+  return false;
+}
+
+struct OperandCompiler {
+  Plan& plan;
+  std::map<std::string, int> leaf_of;
+  bool force_vm = false;
+  bool skip_range_check = false;
+
+  explicit OperandCompiler(Plan& p) : plan(p) {
+    for (size_t i = 0; i < p.leaves.size(); ++i) leaf_of[p.leaves[i].meta.name] = static_cast<int>(i);
+  }
+
+  const LeafInfo& leaf_checked(const std::string& name) {
+    auto it = leaf_of.find(name);
+    if (it == leaf_of.end()) throw error(errc::domain, "no binding for array " + name);
+    return plan.leaves[it->second];
+  }
+
+  int add_chain(const std::vector<CoefFactor>& f) {
+    CoefChain c{};
+    c.n = static_cast<int>(f.size());
+    for (size_t i = 0; i < f.size(); ++i) c.f[i] = f[i];
+    plan.chains.push_back(c);
+    return static_cast<int>(plan.chains.size()) - 1;
+  }
+
+  // factor classification for the affine path
+  enum class FK { scalar, tensor, other };
+  FK classify(const Expr& f, const OperandExpr& op, const ArrayMeta& sm, CoefFactor* cf, int* leaf) {
+    if (f.kind == Expr::Kind::literal) {
+      *cf = CoefFactor{-1, f.literal};
+      return FK::scalar;
+    }
+    if (f.kind != Expr::Kind::access) return FK::other;
+    auto it = leaf_of.find(f.name);
+    if (it == leaf_of.end()) return FK::other;
+    const LeafInfo& L = plan.leaves[it->second];
+    if (f.subs.empty() && L.meta.shape.empty()) {
+      *cf = CoefFactor{it->second, 0.0};
+      return FK::scalar;
+    }
+    if (f.subs == op.params && L.meta.shape == sm.shape &&
+        std::set<std::string>(op.params.begin(), op.params.end()).size() == op.params.size()) {
+      *leaf = it->second;
+      return FK::tensor;
+    }
+    return FK::other;
+  }
+
+  bool try_affine(const OperandExpr& op, const ArrayMeta& sm, OperandStatic& out) {
+    std::vector<std::pair<char, const Expr*>> terms;
+    flatten_chain(op.body, '+', '-', terms);
+    if (terms.size() > static_cast<size_t>(kMaxAffineTerms)) return false;
+    OperandStatic s{};
+    s.kind = OPK_AFFINE;
+    s.leaf = -1;
+    s.ndim = static_cast<int>(op.params.size());
+    s.n_terms = static_cast<int>(terms.size());
+    const size_t chains_before = plan.chains.size();
+    for (size_t t = 0; t < terms.size(); ++t) {
+      std::vector<std::pair<char, const Expr*>> factors;
+      flatten_chain(*terms[t].second, '*', '*', factors);
+      std::vector<CoefFactor> pre, post;
+      int leaf = -1;
+      for (const auto& [opch, fx] : factors) {
+        CoefFactor cf{};
+        int lf = -1;
+        const FK k = classify(*fx, op, sm, &cf, &lf);
+        if (k == FK::other || (k == FK::tensor && leaf >= 0)) {
+          plan.chains.resize(chains_before);
+          return false;
+        }
+        if (k == FK::tensor)
+          leaf = lf;
+        else
+          (leaf < 0 ? pre : post).push_back(cf);
+      }
+      AffineTerm& tm = s.term[t];
+      tm.sign = terms[t].first == '-' ? -1 : 1;
+      tm.leaf = leaf;
+      tm.pre = tm.post0 = tm.post1 = -1;
+      if (pre.size() > static_cast<size_t>(kMaxCoefFactors) || post.size() > 2) {
+        plan.chains.resize(chains_before);
+        return false;
+      }
+      if (!pre.empty()) tm.pre = add_chain(pre);
+      if (!post.empty()) tm.post0 = add_chain({post[0]});
+      if (post.size() > 1) tm.post1 = add_chain({post[1]});
+    }
+    out = s;
+    return true;
+  }
+
+  int emit(const Expr& e, int depth, const OperandExpr& op, const ArrayMeta& sm) {
+    if (depth >= kMaxVmRegs) throw error(errc::usage, "operand expression nests deeper than the device VM's 16 registers");
+    VmInstr in{};
+    in.dst = depth;
+    switch (e.kind) {
+      case Expr::Kind::literal:
+        in.code = VM_LIT;
+        in.imm = e.literal;
+        break;
+      case Expr::Kind::param: {
+        in.code = VM_PARAM;
+        const auto it = std::find(op.params.begin(), op.params.end(), e.name);
+        in.arg = static_cast<int>(it - op.params.begin());
+        break;
+      }
+      case Expr::Kind::access: {
+        const LeafInfo& L = leaf_checked(e.name);
+        if (e.subs.size() != L.meta.shape.size())
+          throw error(errc::domain, "array " + e.name + " read with " + std::to_string(e.subs.size()) +
+                                        " subscripts, has " + std::to_string(L.meta.shape.size()) + " axes");
+        VmRead rd{};
+        rd.leaf = leaf_of.at(e.name);
+        rd.ndim = static_cast<int>(e.subs.size());
+        if (rd.ndim > kMaxDims) throw error(errc::usage, "array " + e.name + " has too many axes for the device VM");
+        std::int64_t stride = 1;
+        for (int d = rd.ndim - 1; d >= 0; --d) {
+          const auto it = std::find(op.params.begin(), op.params.end(), e.subs[d]);
+          rd.param_of[d] = static_cast<int>(it - op.params.begin());
+          rd.stride[d] = stride;
+          stride *= L.meta.shape[d];
+        }
+        plan.reads.push_back(rd);
+        in.code = VM_READ;
+        in.arg = static_cast<int>(plan.reads.size()) - 1;
+        break;
+      }
+      case Expr::Kind::unary: {
+        emit(e.children[0], depth, op, sm);
+        in.a = depth;
+        if (e.name == "sin") in.code = VM_SIN;
+        else if (e.name == "cos") in.code = VM_COS;
+        else if (e.name == "exp") in.code = VM_EXP;
+        else if (e.name == "sqrt") in.code = VM_SQRT;
+        else if (e.name == "reciprocal") in.code = VM_RECIP;
+        else throw error(errc::domain, "unknown function " + e.name);
+        break;
+      }
+      case Expr::Kind::binary: {
+        emit(e.children[0], depth, op, sm);
+        emit(e.children[1], depth + 1, op, sm);
+        in.a = depth;
+        in.b = depth + 1;
+        switch (e.op) {
+          case '+': in.code = VM_ADD; break;
+          case '-': in.code = VM_SUB; break;
+          case '*': in.code = VM_MUL; break;
+          case '/': in.code = VM_DIV; break;
+          default: throw error(errc::domain, std::string("unknown operator ") + e.op);
+        }
+        break;
+      }
+    }
+    plan.prog.push_back(in);
+    return depth;
+  }
+
+  // Reproduce the reference's failure for reads that leave the array: the
+  // first offending point in row-major order over the operand's shape.
+  void check_ranges(const OperandExpr& op, const ArrayMeta& sm) {
+    struct Hit {
+      std::int64_t flat;
+      std::string name;
+      std::int64_t value;
+      size_t axis;
+    };
+    std::optional<Hit> first;
+    std::vector<std::int64_t> pstride(op.params.size(), 1);
+    for (int k = static_cast<int>(op.params.size()) - 2; k >= 0; --k)
+      pstride[k] = pstride[k + 1] * sm.shape[k + 1];
+    std::function<void(const Expr&)> walk = [&](const Expr& e) {
+      for (const Expr& c : e.children) walk(c);
+      if (e.kind != Expr::Kind::access) return;
+      auto it = leaf_of.find(e.name);
+      if (it == leaf_of.end()) return;
+      const ArrayMeta& lm = plan.leaves[it->second].meta;
+      for (size_t d = 0; d < e.subs.size() && d < lm.shape.size(); ++d) {
+        const auto pit = std::find(op.params.begin(), op.params.end(), e.subs[d]);
+        const size_t k = static_cast<size_t>(pit - op.params.begin());
+        if (k >= sm.shape.size() || sm.shape[k] <= lm.shape[d]) continue;
+        const std::int64_t flat = lm.shape[d] * pstride[k];
+        if (!first || flat < first->flat) first = Hit{flat, e.name, lm.shape[d], d};
+      }
+    };
+    walk(op.body);
+    if (first)
+      throw error(errc::domain, "array " + first->name + " subscript " + std::to_string(first->value) +
+                                    " out of range on axis " + std::to_string(first->axis));
+  }
+
+  OperandStatic compile(const OperandExpr& op, const ArrayMeta& sm) {
+    if (op.params.size() != sm.shape.size())
+      throw error(errc::domain, "materialize: operand takes " + std::to_string(op.params.size()) +
+                                    " parameters, shape has " + std::to_string(sm.shape.size()) + " axes");
+    // plain positional read of a same-shaped leaf
+    const Expr& b = op.body;
+    if (!force_vm && b.kind == Expr::Kind::access && b.subs == op.params) {
+      auto it = leaf_of.find(b.name);
+      if (it != leaf_of.end() && plan.leaves[it->second].meta.shape == sm.shape &&
+          std::set<std::string>(op.params.begin(), op.params.end()).size() == op.params.size()) {
+        OperandStatic s{};
+        s.kind = OPK_PLAIN;
+        s.leaf = it->second;
+        s.ndim = static_cast<int>(sm.shape.size());
+        return s;
+      }
+    }
+    // validate every read up front (reference messages)
+    std::function<void(const Expr&)> check = [&](const Expr& e) {
+      for (const Expr& c : e.children) check(c);
+      if (e.kind == Expr::Kind::access) {
+        const LeafInfo& L = leaf_checked(e.name);
+        if (e.subs.size() != L.meta.shape.size())
+          throw error(errc::domain, "array " + e.name + " read with " + std::to_string(e.subs.size()) +
+                                        " subscripts, has " + std::to_string(L.meta.shape.size()) + " axes");
+      }
+    };
+    check(b);
+    if (!skip_range_check) check_ranges(op, sm);
+    OperandStatic s{};
+    if (!force_vm && try_affine(op, sm, s)) return s;
+    s = OperandStatic{};
+    s.kind = OPK_VM;
+    s.ndim = static_cast<int>(sm.shape.size());
+    s.prog_off = static_cast<int>(plan.prog.size());
+    emit(b, 0, op, sm);
+    s.prog_len = static_cast<int>(plan.prog.size()) - s.prog_off;
+    if (uses_sqrt(b)) plan.complex_mode = true;
+    return s;
+  }
+};
+
+// --------------------------------------------------------- pattern matching --
+
+// Match a canonical notation against a role pattern (slots of role letters).
+// Finds a slot permutation and index bijection making them equal position by
+// position; returns role slot -> canonical slot and role letter -> index.
+struct RoleMatch {
+  std::vector<int> slot;            // pattern slot -> canonical slot
+  std::map<char, std::string> idx;  // role letter -> canonical index
+};
+
+std::optional<RoleMatch> match_roles(const BatchedEinsum& c, const std::vector<std::string>& pat_in,
+                                     const std::string& pat_out) {
+  const int n = c.n();
+  if (static_cast<int>(pat_in.size()) != n || c.i_out.size() != pat_out.size()) return std::nullopt;
+  std::vector<int> perm(static_cast<size_t>(n));
+  std::iota(perm.begin(), perm.end(), 0);
+  do {
+    std::map<char, std::string> fwd;
+    std::map<std::string, char> back;
+    bool ok = true;
+    auto bind = [&](char role, const std::string& sym) {
+      auto [it, fresh] = fwd.insert({role, sym});
+      if (!fresh && it->second != sym) return false;
+      auto [jt, fresh2] = back.insert({sym, role});
+      if (!fresh2 && jt->second != role) return false;
+      return true;
+    };
+    for (int k = 0; k < n && ok; ++k) {
+      const std::string& roles = pat_in[k];
+      const auto& syms = c.i_in[perm[k]];
+      if (roles.size() != syms.size()) {
+        ok = false;
+        break;
+      }
+      for (size_t d = 0; d < roles.size() && ok; ++d) ok = bind(roles[d], syms[d]);
+    }
+    for (size_t d = 0; d < pat_out.size() && ok; ++d) ok = bind(pat_out[d], c.i_out[d]);
+    if (ok) return RoleMatch{perm, fwd};
+  } while (std::next_permutation(perm.begin(), perm.end()));
+  return std::nullopt;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
+
+// FEM gradient family: J[x,r,e] D[x,i,j] U[e,j] -> Y[r,e,i]
+bool bind_fem(Plan& p, std::string* why) {
+  const auto m = match_roles(p.canon.canonical, {"xre", "xij", "ej"}, "rei");
+  if (!m) {
+    *why = "notation is not xre,xij,ej->rei";
+    return false;
+  }
+  if (p.complex_mode) {
+    *why = "complex data";
+    return false;
+  }
+  const auto lens = feinsum::index_lengths(p.canon.canonical);
+  FemBinding f;
+  f.NX = static_cast<int>(lens.at(m->idx.at('x')));
+  f.NR = static_cast<int>(lens.at(m->idx.at('r')));
+  f.NI = static_cast<int>(lens.at(m->idx.at('i')));
+  f.NJ = static_cast<int>(lens.at(m->idx.at('j')));
+  f.E = lens.at(m->idx.at('e'));
+  f.rows = p.skel.b();
+  if (!fem_grad_supported(f.NX, f.NR, f.NI, f.NJ)) {
+    *why = "no compiled instance for these extents";
+    return false;
+  }
+  if (f.E % 2 != 0) {
+    *why = "odd element count (bulk copies need 16-byte runs)";
+    return false;
+  }
+  if (f.rows > kFemMaxRows) {
+    *why = "too many rows";
+    return false;
+  }
+  const int n = p.skel.n();
+  int u_tiles = 0;
+  for (int q = 0; q < f.rows; ++q) {
+    const int ur = p.canon.sigma_row[q];
+    auto operand = [&](int role) -> const OperandStatic& {
+      return p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[m->slot[role]]];
+    };
+    const OperandStatic& J = operand(0);
+    const OperandStatic& D = operand(1);
+    const OperandStatic& U = operand(2);
+    if (J.kind != OPK_PLAIN || D.kind != OPK_PLAIN) {
+      *why = "functional J or D operand";
+      return false;
+    }
+    if (p.leaves[J.leaf].storage != ST_F64 || p.leaves[D.leaf].storage != ST_F64) {
+      *why = "non-f64 storage";
+      return false;
+    }
+    std::vector<AffineTerm> terms;
+    if (U.kind == OPK_PLAIN) {
+      terms.push_back(AffineTerm{1, -1, U.leaf, -1, -1});
+    } else if (U.kind == OPK_AFFINE) {
+      for (int t = 0; t < U.n_terms; ++t) {
+        if (U.term[t].leaf < 0 || U.term[t].post1 >= 0) {
+          *why = "affine U operand with a constant or two post factors";
+          return false;
+        }
+        terms.push_back(U.term[t]);
+      }
+    } else {
+      *why = "U operand needs the VM";
+      return false;
+    }
+    for (const auto& t : terms)
+      if (p.leaves[t.leaf].storage != ST_F64) {
+        *why = "non-f64 storage";
+        return false;
+      }
+    u_tiles += static_cast<int>(terms.size());
+    f.j_leaf.push_back(J.leaf);
+    f.d_leaf.push_back(D.leaf);
+    f.u_terms.push_back(std::move(terms));
+    f.out_row.push_back(ur);
+    if (p.outputs[ur].storage != ST_F64) {
+      *why = "non-f64 output";
+      return false;
+    }
+  }
+  if (u_tiles > kFemMaxUTiles) {
+    *why = "too many U tiles";
+    return false;
+  }
+  p.fem = std::move(f);
+  return true;
+}
+
+// ------------------------------------------------------------ path FLOPs --
+
+}  // namespace
+
+double optimal_path_flops(const BatchedEinsum& e) {
+  const int n = e.n();
+  const auto len = feinsum::index_lengths(e);
+  std::vector<std::set<std::string>> idx(static_cast<size_t>(n));
+  for (int k = 0; k < n; ++k) idx[k].insert(e.i_in[k].begin(), e.i_in[k].end());
+  const std::set<std::string> out(e.i_out.begin(), e.i_out.end());
+  auto size_of = [&](const std::set<std::string>& s) {
+    double v = 1;
+    for (const auto& x : s) v *= static_cast<double>(len.at(x));
+    return v;
+  };
+  if (n == 1) {
+    // a single operand: one pass over its iteration space if it reduces
+    std::set<std::string> all = idx[0];
+    const bool reduces = all.size() > out.size() || e.i_in[0].size() != all.size();
+    return reduces ? size_of(all) : 0.0;
+  }
+  if (n > 16) return feinsum::flop_count(e) / std::max(1, e.b());
+  const int full = (1 << n) - 1;
+  std::vector<std::set<std::string>> keep(static_cast<size_t>(full) + 1);
+  for (int s = 1; s <= full; ++s) {
+    std::set<std::string> inside, outside = out;
+    for (int k = 0; k < n; ++k)
+      (s >> k & 1 ? inside : outside).insert(idx[k].begin(), idx[k].end());
+    for (const auto& x : inside)
+      if (outside.count(x)) keep[s].insert(x);
+  }
+  std::vector<double> cost(static_cast<size_t>(full) + 1, 0.0);
+  for (int s = 1; s <= full; ++s) {
+    if ((s & (s - 1)) == 0) continue;  // singleton
+    double best = INFINITY;
+    for (int a = (s - 1) & s; a > 0; a = (a - 1) & s) {
+      const int b = s ^ a;
+      if (a < b) continue;  // each split once
+      std::set<std::string> all = keep[a];
+      all.insert(keep[b].begin(), keep[b].end());
+      const bool summed = all.size() > keep[s].size();
+      const double c = cost[a] + cost[b] + size_of(all) * (summed ? 2.0 : 1.0);
+      best = std::min(best, c);
+    }
+    cost[s] = best;
+  }
+  return cost[full];
+}
+
+namespace {
+
+double expr_ops(const Expr& e) {
+  double c = (e.kind == Expr::Kind::binary || e.kind == Expr::Kind::unary) ? 1.0 : 0.0;
+  for (const Expr& x : e.children) c += expr_ops(x);
+  return c;
+}
+
+void upload_tables(Plan& p, GenericLaunch& g, const BatchedEinsum& e, bool dry_run) {
+  std::map<std::string, int> pos;
+  {
+    std::vector<std::string> syms = e.i_out;
+    for (auto& s : feinsum::reduction_indices(e)) syms.push_back(s);
+    for (size_t i = 0; i < syms.size(); ++i) pos[syms[i]] = static_cast<int>(i);
+  }
+  // static blob: ops | slot_pos | slot_stride | slot_ndim | prog | reads | chains
+  std::vector<int> slot_pos(static_cast<size_t>(e.n()) * kMaxDims, 0), slot_ndim(static_cast<size_t>(e.n()), 0);
+  std::vector<std::int64_t> slot_stride(static_cast<size_t>(e.n()) * kMaxDims, 0);
+  for (int k = 0; k < e.n(); ++k) {
+    const int nd = static_cast<int>(e.i_in[k].size());
+    if (nd > kMaxDims) throw error(errc::usage, "operand with more than 12 axes");
+    slot_ndim[k] = nd;
+    std::int64_t st = 1;
+    for (int d = nd - 1; d >= 0; --d) {
+      slot_pos[k * kMaxDims + d] = pos.at(e.i_in[k][d]);
+      slot_stride[k * kMaxDims + d] = st;
+      st *= e.args[0][k].shape[d];
+    }
+  }
+  auto align = [](size_t x) { return (x + 255) & ~size_t{255}; };
+  size_t off = 0;
+  const size_t o_ops = off; off = align(off + sizeof(OperandStatic) * p.ops.size());
+  const size_t o_pos = off; off = align(off + sizeof(int) * slot_pos.size());
+  const size_t o_str = off; off = align(off + sizeof(std::int64_t) * slot_stride.size());
+  const size_t o_nd = off; off = align(off + sizeof(int) * slot_ndim.size());
+  const size_t o_prog = off; off = align(off + sizeof(VmInstr) * p.prog.size());
+  const size_t o_reads = off; off = align(off + sizeof(VmRead) * p.reads.size());
+  const size_t o_chains = off; off = align(off + sizeof(CoefChain) * p.chains.size());
+  const size_t total = std::max<size_t>(off, 256);
+  std::vector<unsigned char> blob(total, 0);
+  auto put = [&](size_t at, const void* src, size_t n) {
+    if (n) std::memcpy(blob.data() + at, src, n);
+  };
+  put(o_ops, p.ops.data(), sizeof(OperandStatic) * p.ops.size());
+  put(o_pos, slot_pos.data(), sizeof(int) * slot_pos.size());
+  put(o_str, slot_stride.data(), sizeof(std::int64_t) * slot_stride.size());
+  put(o_nd, slot_ndim.data(), sizeof(int) * slot_ndim.size());
+  put(o_prog, p.prog.data(), sizeof(VmInstr) * p.prog.size());
+  put(o_reads, p.reads.data(), sizeof(VmRead) * p.reads.size());
+  put(o_chains, p.chains.data(), sizeof(CoefChain) * p.chains.size());
+
+  if (dry_run) return;
+  cuda_check(cudaGetDevice(&p.device), "cudaGetDevice");
+  cuda_check(device_sm_count(&p.sm_count), "device attributes");
+  cuda_check(cudaMalloc(&p.d_blob, total), "cudaMalloc(plan tables)");
+  cuda_check(cudaMemcpy(p.d_blob, blob.data(), total, cudaMemcpyHostToDevice), "upload plan tables");
+  if (!p.chains.empty())
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_coef), sizeof(double) * 2 * p.chains.size()),
+               "cudaMalloc(coefficients)");
+  auto* base = static_cast<unsigned char*>(p.d_blob);
+  g.ops = reinterpret_cast<const OperandStatic*>(base + o_ops);
+  g.slot_pos = reinterpret_cast<const int*>(base + o_pos);
+  g.slot_stride = reinterpret_cast<const std::int64_t*>(base + o_str);
+  g.slot_ndim = reinterpret_cast<const int*>(base + o_nd);
+  g.prog = reinterpret_cast<const VmInstr*>(base + o_prog);
+  g.reads = reinterpret_cast<const VmRead*>(base + o_reads);
+  g.chains = reinterpret_cast<const CoefChain*>(base + o_chains);
+  g.n_chains = static_cast<int>(p.chains.size());
+  g.coef = p.d_coef;
+}
+
+void finish_plan(Plan& p, const PlanOptions& opt) {
+  const BatchedEinsum& e = p.skel;
+  if (e.b() > kMaxRows) throw error(errc::usage, "more than 96 rows; spell the batch as an index");
+  if (p.leaves.size() > static_cast<size_t>(kMaxLeaves)) throw error(errc::usage, "more than 96 input arrays");
+
+  // outputs: R<row>, widest dtype of the row, i_out shape
+  const auto lens = feinsum::index_lengths(e);
+  for (int r = 0; r < e.b(); ++r) {
+    OutputInfo o;
+    o.meta.name = "R" + std::to_string(r + 1);
+    o.meta.dtype = e.args[r][0].dtype;
+    for (const auto& a : e.args[r])
+      if (feinsum::dtype_rank(a.dtype) > feinsum::dtype_rank(o.meta.dtype)) o.meta.dtype = a.dtype;
+    for (const auto& s : e.i_out) o.meta.shape.push_back(lens.at(s));
+    if (opt.storage == "wide")
+      o.storage = p.complex_mode ? ST_C128 : ST_F64;
+    else
+      o.storage = native_storage(o.meta.dtype);
+    p.outputs.push_back(o);
+  }
+
+  // costs
+  const double row_flops = optimal_path_flops(e);
+  p.alg_flops = row_flops * e.b();
+  p.ref_flops = feinsum::flop_count(e);
+  p.operand_flops = 0;
+  if (p.functional)
+    for (const auto& [name, op] : p.operand_exprs) {
+      std::int64_t count = 1;
+      for (const auto& row : e.args)
+        for (const auto& a : row)
+          if (a.name == name) count = a.num_elements();
+      p.operand_flops += expr_ops(op.body) * static_cast<double>(count);
+    }
+  p.alg_flops += p.operand_flops;
+  p.bytes = 0;
+  for (const auto& L : p.leaves) p.bytes += static_cast<double>(L.bytes());
+  for (const auto& o : p.outputs) p.bytes += static_cast<double>(o.bytes());
+
+  // normal form + key (0-dim operands cannot be encoded: generic path)
+  bool encodable = opt.canonicalize;
+  for (const auto& a : feinsum::universe(e))
+    if (a.dim() == 0) encodable = false;
+  if (encodable) {
+    // memo keyed by the exact spelling: repeated plans skip the search
+    static std::mutex mu;
+    static std::map<std::string, CanonResult> memo;
+    const std::string spelling = fejson::dump(feinsum::transport::einsum_to_json(e));
+    bool hit = false;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      auto it = memo.find(spelling);
+      if (it != memo.end()) {
+        p.canon = it->second;
+        hit = true;
+      }
+    }
+    if (!hit) {
+      p.canon = feinsum::canonicalize(e);
+      std::lock_guard<std::mutex> lock(mu);
+      if (memo.size() > 4096) memo.clear();
+      memo.emplace(spelling, p.canon);
+    }
+    p.key = feinsum::detail::key_of_canonical(p.canon.canonical);
+    p.has_canon = true;
+  }
+
+  // kernel choice: forced > fact > first matching family > generic
+  std::vector<Family> order = {Family::fem_grad};
+  auto family_of = [](const std::string& t) -> std::optional<Family> {
+    for (Family f : {Family::generic, Family::fem_grad, Family::gett, Family::tt, Family::hex})
+      if (t == family_transform(f)) return f;
+    return std::nullopt;
+  };
+  std::string why;
+  auto try_bind = [&](Family f) -> bool {
+    if (!p.has_canon) return f == Family::generic;
+    switch (f) {
+      case Family::generic: return true;
+      case Family::fem_grad: return bind_fem(p, &why);
+      default: return false;
+    }
+  };
+  p.family = Family::generic;
+  p.source = "fallback";
+  if (!opt.force_transform.empty()) {
+    auto f = family_of(opt.force_transform);
+    if (!f) throw error(errc::usage, "unknown transform " + opt.force_transform);
+    if (!try_bind(*f)) throw error(errc::usage, "transform " + opt.force_transform + " does not apply: " + why);
+    p.family = *f;
+    p.source = "forced";
+  } else {
+    std::optional<feinsum::FactRecord> fact;
+    if (p.has_canon)
+      fact = facts_index().best(opt.facts_path.empty() ? default_facts_path() : opt.facts_path, p.key, opt.device_id);
+    if (fact) {
+      auto f = family_of(fact->transform_id);
+      if (f && try_bind(*f)) {
+        p.family = *f;
+        p.source = "fact";
+        p.meta = fact->meta;
+      }
+    }
+    if (p.source != "fact")
+      for (Family f : order)
+        if (try_bind(f)) {
+          p.family = f;
+          p.source = "default";
+          break;
+        }
+  }
+  p.transform = family_transform(p.family);
+
+  // generic launch (always prepared: it is also the runtime fallback)
+  std::vector<std::string> syms = e.i_out;
+  for (auto& s : feinsum::reduction_indices(e)) syms.push_back(s);
+  if (syms.size() > static_cast<size_t>(kMaxSyms)) throw error(errc::usage, "more than 32 distinct indices");
+  GenericLaunch& g = p.gen;
+  g = GenericLaunch{};
+  g.n_syms = static_cast<int>(syms.size());
+  g.n_out = static_cast<int>(e.i_out.size());
+  g.b = e.b();
+  g.n = e.n();
+  g.out_points = 1;
+  g.red_points = 1;
+  for (size_t i = 0; i < syms.size(); ++i) {
+    g.extent[i] = lens.at(syms[i]);
+    (static_cast<int>(i) < g.n_out ? g.out_points : g.red_points) *= g.extent[i];
+  }
+  g.complex_mode = p.complex_mode;
+  for (int r = 0; r < e.b(); ++r) g.out_storage[r] = p.outputs[r].storage;
+
+  upload_tables(p, g, e, opt.dry_run);
+}
+
+int leaf_storage_for(const ArrayMeta& m, const PlanOptions& opt) {
+  auto it = opt.storage_of.find(m.name);
+  if (it != opt.storage_of.end()) return storage_from_name(it->second);
+  if (opt.storage == "wide") return is_complex_dtype(m.dtype) ? ST_C128 : ST_F64;
+  return native_storage(m.dtype);
+}
+
+}  // namespace
+
+Plan::~Plan() {
+  if (d_blob) cudaFree(d_blob);
+  if (d_coef) cudaFree(d_coef);
+}
+
+std::unique_ptr<Plan> make_plan(const BatchedEinsum& e, const PlanOptions& opt) {
+  feinsum::require_valid(e);
+  auto p = std::make_unique<Plan>();
+  p->skel = e;
+  for (const auto& m : feinsum::universe(e)) {
+    LeafInfo L{m, leaf_storage_for(m, opt)};
+    if (storage_complex(L.storage)) p->complex_mode = true;
+    p->leaves.push_back(L);
+  }
+  std::map<std::string, int> leaf_of;
+  for (size_t i = 0; i < p->leaves.size(); ++i) leaf_of[p->leaves[i].meta.name] = static_cast<int>(i);
+  for (int r = 0; r < e.b(); ++r)
+    for (int k = 0; k < e.n(); ++k) {
+      OperandStatic s{};
+      s.kind = OPK_PLAIN;
+      s.leaf = leaf_of.at(e.args[r][k].name);
+      s.ndim = e.args[r][k].dim();
+      p->ops.push_back(s);
+    }
+  finish_plan(*p, opt);
+  return p;
+}
+
+std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,
+                                           const std::map<std::string, OperandExpr>& operands,
+                                           const std::map<std::string, ArrayMeta>& arrays, const PlanOptions& opt) {
+  feinsum::require_valid(skeleton);
+  auto p = std::make_unique<Plan>();
+  p->skel = skeleton;
+  p->functional = true;
+  p->operand_exprs = operands;
+  for (const auto& [name, m] : arrays) {
+    LeafInfo L{m, leaf_storage_for(m, opt)};
+    if (storage_complex(L.storage)) p->complex_mode = true;
+    p->leaves.push_back(L);
+  }
+  OperandCompiler cc(*p);
+  cc.force_vm = opt.force_vm;
+  cc.skip_range_check = opt.skip_range_check;
+  std::map<std::string, OperandStatic> compiled;
+  for (const auto& m : feinsum::universe(skeleton)) {
+    auto it = operands.find(m.name);
+    if (it == operands.end()) throw error(errc::domain, "no operand expression for " + m.name);
+    compiled[m.name] = cc.compile(it->second, m);
+  }
+  for (int r = 0; r < skeleton.b(); ++r)
+    for (int k = 0; k < skeleton.n(); ++k) p->ops.push_back(compiled.at(skeleton.args[r][k].name));
+  finish_plan(*p, opt);
+  return p;
+}
+
+void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream) {
+  GenericLaunch g = plan.gen;
+  for (size_t i = 0; i < plan.leaves.size(); ++i) {
+    g.leaves.ptr[i] = d_in[i];
+    g.leaves.storage[i] = plan.leaves[i].storage;
+  }
+  for (int r = 0; r < plan.skel.b(); ++r) g.out[r] = d_out[r];
+  if (!plan.chains.empty())
+    cuda_check(launch_coef(g.chains, g.n_chains, g.leaves, plan.d_coef, stream), "coefficient kernel");
+
+  if (plan.family == Family::fem_grad) {
+    const FemBinding& f = plan.fem;
+    FemGradLaunch L{};
+    L.rows = f.rows;
+    L.E = f.E;
+    L.NX = f.NX;
+    L.NR = f.NR;
+    L.NI = f.NI;
+    L.NJ = f.NJ;
+    L.stages = 4;
+    std::vector<int> jl, dl;
+    bool ok = true;
+    int u = 0;
+    L.plain_u = true;
+    for (int q = 0; q < f.rows; ++q) {
+      auto idx_of = [](std::vector<int>& v, int leaf) {
+        auto it = std::find(v.begin(), v.end(), leaf);
+        if (it != v.end()) return static_cast<int>(it - v.begin());
+        v.push_back(leaf);
+        return static_cast<int>(v.size()) - 1;
+      };
+      L.row_j[q] = idx_of(jl, f.j_leaf[q]);
+      L.row_d[q] = idx_of(dl, f.d_leaf[q]);
+      L.row_u_first[q] = u;
+      L.row_u_count[q] = static_cast<int>(f.u_terms[q].size());
+      if (f.u_terms[q].size() != 1 || f.u_terms[q][0].pre >= 0 || f.u_terms[q][0].post0 >= 0) L.plain_u = false;
+      for (const AffineTerm& t : f.u_terms[q]) {
+        L.U[u] = static_cast<const double*>(d_in[t.leaf]);
+        L.u_sign[u] = t.sign;
+        L.u_pre[u] = t.pre;
+        L.u_post[u] = t.post0;
+        ok = ok && aligned16(L.U[u]);
+        ++u;
+      }
+      L.Y[q] = static_cast<double*>(d_out[f.out_row[q]]);
+    }
+    L.n_u = u;
+    L.n_j = static_cast<int>(jl.size());
+    L.n_d = static_cast<int>(dl.size());
+    for (size_t a = 0; a < jl.size(); ++a) {
+      L.J[a] = static_cast<const double*>(d_in[jl[a]]);
+      ok = ok && aligned16(L.J[a]);
+    }
+    for (size_t a = 0; a < dl.size(); ++a) L.D[a] = static_cast<const double*>(d_in[dl[a]]);
+    L.coef = plan.d_coef;
+    const int te = f.NI == 10 ? 32 : (f.NI == 4 ? 64 : 16);
+    const std::int64_t ntiles = (f.E + te - 1) / te;
+    L.tile_e = te;
+    L.grid = static_cast<int>(std::min<std::int64_t>(ntiles, static_cast<std::int64_t>(plan.sm_count) * 2));
+    if (ok) {
+      cuda_check(launch_fem_grad(L, stream), "fem_grad kernel");
+      return;
+    }
+  }
+  cuda_check(launch_generic(g, stream), "generic kernel");
+}
+
+void tabulate(const Plan& plan, const std::string& name, const void* const* d_in, double* d_out, std::int64_t first,
+              std::int64_t count, void* stream) {
+  const auto& e = plan.skel;
+  int row = -1, slot = -1;
+  ArrayMeta meta;
+  for (int r = 0; r < e.b() && row < 0; ++r)
+    for (int k = 0; k < e.n(); ++k)
+      if (e.args[r][k].name == name) {
+        row = r;
+        slot = k;
+        meta = e.args[r][k];
+        break;
+      }
+  if (row < 0) throw error(errc::domain, "no operand named " + name);
+  TabulateLaunch t{};
+  t.op = plan.gen.ops + (static_cast<size_t>(row) * e.n() + slot);
+  t.prog = plan.gen.prog;
+  t.reads = plan.gen.reads;
+  t.chains = plan.gen.chains;
+  t.n_chains = plan.gen.n_chains;
+  t.coef = plan.d_coef;
+  t.ndim = meta.dim();
+  for (int d = 0; d < meta.dim(); ++d) t.shape[d] = meta.shape[d];
+  t.first = first;
+  t.count = count;
+  t.complex_mode = plan.complex_mode;
+  for (size_t i = 0; i < plan.leaves.size(); ++i) {
+    t.leaves.ptr[i] = d_in[i];
+    t.leaves.storage[i] = plan.leaves[i].storage;
+  }
+  t.out = d_out;
+  if (!plan.chains.empty())
+    cuda_check(launch_coef(t.chains, t.n_chains, t.leaves, plan.d_coef, stream), "coefficient kernel");
+  cuda_check(launch_tabulate(t, stream), "tabulate kernel");
+}
+
+std::string describe(const Plan& p) {
+  using fejson::Value;
+  Value v = Value::obj();
+  v.set("key", Value::str(p.key));
+  v.set("transform", Value::str(p.transform));
+  v.set("source", Value::str(p.source));
+  v.set("meta", Value::str(p.meta));
+  v.set("functional", Value::boolean_(p.functional));
+  v.set("complex", Value::boolean_(p.complex_mode));
+  Value leaves = Value::arr();
+  for (const auto& L : p.leaves) {
+    Value x = feinsum::transport::meta_to_json(L.meta);
+    x.set("storage", Value::str(storage_name(L.storage)));
+    x.set("bytes", Value::num(L.bytes()));
+    leaves.push(std::move(x));
+  }
+  v.set("inputs", std::move(leaves));
+  Value outs = Value::arr();
+  for (const auto& o : p.outputs) {
+    Value x = feinsum::transport::meta_to_json(o.meta);
+    x.set("storage", Value::str(storage_name(o.storage)));
+    x.set("bytes", Value::num(o.bytes()));
+    outs.push(std::move(x));
+  }
+  v.set("outputs", std::move(outs));
+  v.set("algorithmic_flops", Value::dbl(p.alg_flops));
+  v.set("operand_flops", Value::dbl(p.operand_flops));
+  v.set("reference_flops", Value::dbl(p.ref_flops));
+  v.set("bytes", Value::dbl(p.bytes));
+  if (p.has_canon) {
+    Value c = Value::obj();
+    c.set("canonical", feinsum::transport::einsum_to_json(p.canon.canonical));
+    c.set("sigma_idx", feinsum::transport::strmap_to_json(p.canon.sigma_idx));
+    c.set("sigma_arg", feinsum::transport::strmap_to_json(p.canon.sigma_arg));
+    c.set("sigma_row", feinsum::transport::ints_to_json(p.canon.sigma_row));
+    c.set("sigma_slot", feinsum::transport::ints_to_json(p.canon.sigma_slot));
+    v.set("canon", std::move(c));
+  }
+  if (p.family == Family::fem_grad) {
+    Value f = Value::obj();
+    f.set("NX", Value::num(p.fem.NX));
+    f.set("NR", Value::num(p.fem.NR));
+    f.set("NI", Value::num(p.fem.NI));
+    f.set("NJ", Value::num(p.fem.NJ));
+    f.set("E", Value::num(p.fem.E));
+    v.set("roles", std::move(f));
+  }
+  return fejson::dump(v);
+}
+
+std::unique_ptr<Plan> make_shard(const Plan& full, int rank, int world, const PlanOptions& opt, std::int64_t* lo,
+                                 std::int64_t* hi, std::string* axis) {
+  (void)full;
+  (void)rank;
+  (void)world;
+  (void)opt;
+  (void)lo;
+  (void)hi;
+  (void)axis;
+  throw error(errc::usage, "sharding not implemented yet");
+}
+
+}  // namespace feb200

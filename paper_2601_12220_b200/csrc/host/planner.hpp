@@ -1,0 +1,142 @@
+// B200 planner: turns a (functional) batched einsum into an executable plan.
+//
+//   parse -> validate -> canonicalize (normal form + sigma maps)
+//         -> canonical key -> tuning facts (device "b200")
+//         -> kernel family matched on the canonical form, operands routed to
+//            the caller's buffers by the sigma maps (pointer permutation only)
+//         -> sm_100a launch
+//
+// Functional operands are compiled once per plan into device programs
+// (affine fast path or a register VM) that the kernels evaluate in their
+// operand prologue. Every plan also carries the generic-kernel launch so any
+// einsum runs on the GPU; there is no host evaluation path.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "feinsum/canonicalize.hpp"
+#include "feinsum/core.hpp"
+#include "feinsum/factsdb.hpp"
+#include "feinsum/raising.hpp"
+#include "../kernels/launch.h"
+
+namespace feb200 {
+
+using feinsum::ArrayMeta;
+using feinsum::BatchedEinsum;
+using feinsum::CanonResult;
+using feinsum::Dtype;
+using feinsum::OperandExpr;
+
+enum class Family { generic, fem_grad, gett, tt, hex };
+const char* family_transform(Family f);  // "generic/v1", "fem_grad/v1", ...
+
+struct PlanOptions {
+  std::string storage = "native";              // "native" | "wide"
+  std::map<std::string, std::string> storage_of;  // per-leaf override: f64 c128 f32 c64 ...
+  std::string facts_path;                     // default: bundled facts/b200.facts
+  std::string device_id = "b200";
+  std::string force_transform;                // e.g. "generic/v1"
+  bool canonicalize = true;
+  bool force_vm = false;      // internal: point evaluation (eval_expr)
+  bool skip_range_check = false;
+  bool dry_run = false;       // plan without touching the device (CPU tests)
+};
+
+PlanOptions parse_options(const std::string& json);
+
+struct LeafInfo {
+  ArrayMeta meta;
+  int storage;
+  std::int64_t bytes() const { return meta.num_elements() * storage_bytes(storage); }
+};
+
+struct OutputInfo {
+  ArrayMeta meta;  // name R<row>, widest dtype of the row, shape of i_out
+  int storage;
+  std::int64_t bytes() const { return meta.num_elements() * storage_bytes(storage); }
+};
+
+// Roles of the FEM-gradient family bound to the caller's operands.
+struct FemBinding {
+  int NX, NR, NI, NJ;
+  std::int64_t E;
+  int rows;
+  // per canonical row: leaf indices / output row
+  std::vector<int> j_leaf, d_leaf, out_row;
+  std::vector<std::vector<AffineTerm>> u_terms;  // per row; leaf indices
+};
+
+struct Plan {
+  // ---- what is computed ----
+  BatchedEinsum skel;  // the caller's einsum (skeleton if functional)
+  bool functional = false;
+  std::map<std::string, OperandExpr> operand_exprs;  // functional: skeleton name -> expr
+  std::vector<LeafInfo> leaves;    // execution inputs, in order
+  std::vector<OutputInfo> outputs; // one per caller row, in caller row order
+  std::vector<OperandStatic> ops;  // [row * n + slot], caller order
+  std::vector<VmInstr> prog;
+  std::vector<VmRead> reads;
+  std::vector<CoefChain> chains;
+  bool complex_mode = false;
+
+  // ---- normal form and retrieval ----
+  bool has_canon = false;
+  CanonResult canon;
+  std::string key;
+  std::string transform;  // chosen kernel family
+  std::string meta;       // tuned parameters (fact meta or defaults)
+  std::string source;     // "fact" | "default" | "forced" | "fallback"
+  Family family = Family::generic;
+  FemBinding fem;
+
+  // ---- costs ----
+  double alg_flops = 0, operand_flops = 0, bytes = 0, ref_flops = 0;
+
+  // ---- device state ----
+  int device = 0;
+  void* d_blob = nullptr;
+  double* d_coef = nullptr;
+  GenericLaunch gen{};  // pointers filled per execution
+  int sm_count = 148;
+
+  ~Plan();
+};
+
+std::unique_ptr<Plan> make_plan(const BatchedEinsum& e, const PlanOptions& opt);
+std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,
+                                           const std::map<std::string, OperandExpr>& operands,
+                                           const std::map<std::string, ArrayMeta>& arrays,
+                                           const PlanOptions& opt);
+
+// Enqueue the plan on `stream` with device pointers (inputs in plan->leaves
+// order, outputs in caller row order). Stream-ordered, allocation-free.
+void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream);
+
+// Shard plan for rank/world along the family's shard axis.
+std::unique_ptr<Plan> make_shard(const Plan& full, int rank, int world, const PlanOptions& opt,
+                                 std::int64_t* lo, std::int64_t* hi, std::string* axis);
+
+std::string describe(const Plan& plan);  // JSON
+
+// Algorithmic FLOPs of one row: cheapest pairwise contraction order.
+double optimal_path_flops(const BatchedEinsum& e);
+
+// Tabulate one operand program on the device (materialize / eval_expr).
+void tabulate(const Plan& plan, const std::string& skeleton_name, const void* const* d_in, double* d_out,
+              std::int64_t first, std::int64_t count, void* stream);
+
+// Storage code <-> name ("f64", "c128", ...), and the native storage of a dtype.
+int storage_from_name(const std::string& s);
+const char* storage_name(int st);
+int native_storage(Dtype t);
+
+// Bundled facts file path (next to the shared library).
+std::string default_facts_path();
+
+}  // namespace feb200

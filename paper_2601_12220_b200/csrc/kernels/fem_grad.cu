@@ -1,0 +1,207 @@
+// K1 — batched FEM gradient  y_q[r,e,i] = sum_{x,j} J_q[x,r,e] D_q[x,i,j] U_q[e,j]
+// (the C1/C5 configs), HBM-bound, fp64.
+//
+// B200 design (persistent, warp-specialised, TMA-fed):
+//   * grid = a multiple of the SM count; each CTA walks element tiles of TE
+//     elements with a stride of gridDim.x;
+//   * warp 0 (one elected lane) is the producer: for every tile it arms the
+//     stage's mbarrier with the byte count and issues 1-D bulk copies
+//     (cp.async.bulk, the TMA engine's non-tensor path) of the J tile (NX*NR
+//     contiguous runs of TE doubles per distinct J) and of every U leaf tile
+//     (TE*NJ contiguous doubles) into an S-stage shared-memory ring — inputs are
+//     read from HBM exactly once and shared J is staged once for all rows;
+//   * TE*NI consumer threads, thread (el, i): D_q[x,i,:] lives in registers
+//     (loaded once from a shared copy of D), U is read as double2 broadcasts,
+//     J as broadcasts; t[x] = D.u then y[r] = J^T t. Consecutive threads own
+//     consecutive (e, i), so every y_q[r, :, :] store is a fully coalesced
+//     256-byte warp transaction — no output staging needed;
+//   * functional U operands (e.g. s = u + 0.5 k, the C5 wave step) are fused:
+//     the producer stages each leaf tile and consumers combine them in
+//     registers, so s never exists in HBM (the K2 prologue).
+// The operation order differs from the reference's (factorised contraction
+// path with FMA); parity is within 1e-12 relative.
+#include <cuda_runtime.h>
+
+#include "launch.h"
+#include "ptx.cuh"
+
+namespace feb200 {
+
+namespace {
+
+template <int NX, int NR, int NI, int NJ, int TE, bool kPlainU>
+__global__ void __launch_bounds__(32 + TE * NI, 1)
+    fem_grad_kernel(const __grid_constant__ FemGradLaunch p) {
+  constexpr int kConsumers = TE * NI;
+  static_assert(kConsumers % 32 == 0, "consumer threads must fill warps");
+  constexpr int kConsumerWarps = kConsumers / 32;
+  static_assert(NJ % 2 == 0, "U rows are read as double2");
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int S = p.stages;
+  const int j_tile = NX * NR * TE;        // doubles per distinct J per stage
+  const int u_tile = TE * NJ;             // doubles per U leaf per stage
+  const int stage_doubles = p.n_j * j_tile + p.n_u * u_tile;
+  double* dsm = reinterpret_cast<double*>(smem_raw);                 // D copies
+  double* ring = dsm + p.n_d * NX * NI * NJ;                          // stages
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(ring + static_cast<size_t>(S) * stage_doubles);
+  std::uint64_t* empty = full + S;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const std::int64_t E = p.E;
+  const std::int64_t ntiles = (E + TE - 1) / TE;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], kConsumerWarps);
+    }
+    ptx::fence_barrier_init();
+  }
+  // D arrays to shared memory (tiny, L2-resident across CTAs)
+  for (int t = tid; t < p.n_d * NX * NI * NJ; t += blockDim.x) {
+    const int which = t / (NX * NI * NJ);
+    dsm[t] = __ldg(p.D[which] + (t - which * NX * NI * NJ));
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------ producer ------------------------------
+    if (!ptx::elect_one()) return;
+    const std::uint64_t pol = ptx::policy_evict_first();
+    int it = 0;
+    for (std::int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int s = it % S;
+      const std::uint32_t round = static_cast<std::uint32_t>(it / S);
+      ptx::mbar_wait(&empty[s], (round & 1u) ^ 1u);
+      const std::int64_t e0 = tile * TE;
+      const int cnt = static_cast<int>(E - e0 < TE ? E - e0 : TE);
+      const std::uint32_t jb = static_cast<std::uint32_t>(cnt) * 8u;
+      const std::uint32_t ub = static_cast<std::uint32_t>(cnt) * NJ * 8u;
+      ptx::mbar_arrive_expect_tx(&full[s], static_cast<std::uint32_t>(p.n_j * NX * NR) * jb +
+                                               static_cast<std::uint32_t>(p.n_u) * ub);
+      double* st = ring + static_cast<size_t>(s) * stage_doubles;
+      for (int a = 0; a < p.n_j; ++a)
+        for (int xr = 0; xr < NX * NR; ++xr)
+          ptx::bulk_g2s_hint(st + a * j_tile + xr * TE, p.J[a] + xr * E + e0, jb, &full[s], pol);
+      double* su = st + p.n_j * j_tile;
+      for (int u = 0; u < p.n_u; ++u)
+        ptx::bulk_g2s_hint(su + u * u_tile, p.U[u] + e0 * NJ, ub, &full[s], pol);
+    }
+    return;
+  }
+
+  // -------------------------------- consumers --------------------------------
+  const int c = tid - 32;
+  const int el = c / NI;
+  const int i = c - el * NI;
+  double dreg[NX][NJ];
+  int cur_d = -1;
+  int it = 0;
+  for (std::int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it % S;
+    const std::uint32_t round = static_cast<std::uint32_t>(it / S);
+    ptx::mbar_wait(&full[s], round & 1u);
+    const std::int64_t e0 = tile * TE;
+    const bool live = e0 + el < E;
+    const double* st = ring + static_cast<size_t>(s) * stage_doubles;
+    const double* su = st + p.n_j * j_tile;
+    if (live) {
+      for (int q = 0; q < p.rows; ++q) {
+        if (p.row_d[q] != cur_d) {
+          cur_d = p.row_d[q];
+          const double* dq = dsm + cur_d * NX * NI * NJ;
+#pragma unroll
+          for (int x = 0; x < NX; ++x)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) dreg[x][j] = dq[(x * NI + i) * NJ + j];
+        }
+        double t[NX];
+#pragma unroll
+        for (int x = 0; x < NX; ++x) t[x] = 0.0;
+        const int u0 = p.row_u_first[q];
+#pragma unroll
+        for (int j = 0; j < NJ; j += 2) {
+          double2 u;
+          if (kPlainU) {
+            u = *reinterpret_cast<const double2*>(su + u0 * u_tile + el * NJ + j);
+          } else {
+            u = make_double2(0.0, 0.0);
+            for (int k = 0; k < p.row_u_count[q]; ++k) {
+              const int ut = u0 + k;
+              double2 v = *reinterpret_cast<const double2*>(su + ut * u_tile + el * NJ + j);
+              if (p.u_pre[ut] >= 0) {
+                const double c0 = __ldg(p.coef + 2 * p.u_pre[ut]);
+                v.x = __dmul_rn(c0, v.x);
+                v.y = __dmul_rn(c0, v.y);
+              }
+              if (p.u_post[ut] >= 0) {
+                const double c1 = __ldg(p.coef + 2 * p.u_post[ut]);
+                v.x = __dmul_rn(v.x, c1);
+                v.y = __dmul_rn(v.y, c1);
+              }
+              if (k == 0) {
+                u = v;
+              } else if (p.u_sign[ut] > 0) {
+                u.x = __dadd_rn(u.x, v.x);
+                u.y = __dadd_rn(u.y, v.y);
+              } else {
+                u.x = __dsub_rn(u.x, v.x);
+                u.y = __dsub_rn(u.y, v.y);
+              }
+            }
+          }
+#pragma unroll
+          for (int x = 0; x < NX; ++x) {
+            t[x] = fma(dreg[x][j], u.x, t[x]);
+            t[x] = fma(dreg[x][j + 1], u.y, t[x]);
+          }
+        }
+        const double* jt = st + p.row_j[q] * j_tile;
+        double* yq = p.Y[q];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          double y = 0.0;
+#pragma unroll
+          for (int x = 0; x < NX; ++x) y = fma(jt[(x * NR + r) * TE + el], t[x], y);
+          __stcs(yq + (static_cast<std::int64_t>(r) * E + e0 + el) * NI + i, y);
+        }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) ptx::mbar_arrive(&empty[s]);
+  }
+}
+
+template <int NX, int NR, int NI, int NJ, int TE>
+int launch_shape(const FemGradLaunch& p, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (static_cast<size_t>(p.n_d) * NX * NI * NJ +
+                                        static_cast<size_t>(p.stages) * (p.n_j * NX * NR * TE + p.n_u * TE * NJ)) +
+                      sizeof(std::uint64_t) * 2 * p.stages;
+  auto run = [&](auto kern) -> int {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<p.grid, 32 + TE * NI, smem, s>>>(p);
+    return cudaGetLastError();
+  };
+  if (p.plain_u) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true>);
+  return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false>);
+}
+
+}  // namespace
+
+bool fem_grad_supported(int NX, int NR, int NI, int NJ) {
+  return NX == 3 && NR == 3 && ((NI == 10 && NJ == 10) || (NI == 4 && NJ == 4) || (NI == 20 && NJ == 20));
+}
+
+int launch_fem_grad(const FemGradLaunch& p, void* stream) {
+  if (p.E == 0) return cudaSuccess;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p.NI == 10 && p.NJ == 10) return launch_shape<3, 3, 10, 10, 32>(p, s);
+  if (p.NI == 4 && p.NJ == 4) return launch_shape<3, 3, 4, 4, 64>(p, s);
+  if (p.NI == 20 && p.NJ == 20) return launch_shape<3, 3, 20, 20, 16>(p, s);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace feb200

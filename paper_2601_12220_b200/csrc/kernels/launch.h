@@ -1,0 +1,255 @@
+// Host <-> device launch contracts of the sm_100a kernels. Plain C++ structs
+// (no CUDA headers) shared by the planner (host .cpp) and the kernels (.cu).
+// The planner fills these from a Plan; each launch_* function enqueues its
+// kernel(s) on the given stream and returns a cudaError_t as int.
+#pragma once
+
+#include <cstdint>
+
+namespace feb200 {
+
+// Device storage of an array. NATIVE storage follows the declared dtype; the
+// DenseArray drop-in uploads "wide" (F64/C128) so values survive unrounded,
+// exactly as the reference holds them (complex<double> for every dtype).
+enum Storage : int {
+  ST_F64 = 0,
+  ST_F32 = 1,
+  ST_C128 = 2,
+  ST_C64 = 3,
+  ST_I8 = 4,
+  ST_I32 = 5,
+  ST_I64 = 6,
+  ST_F16 = 7,
+};
+
+inline int storage_bytes(int s) {
+  switch (s) {
+    case ST_F64: return 8;
+    case ST_F32: return 4;
+    case ST_C128: return 16;
+    case ST_C64: return 8;
+    case ST_I8: return 1;
+    case ST_I32: return 4;
+    case ST_I64: return 8;
+    case ST_F16: return 2;
+  }
+  return 0;
+}
+inline bool storage_complex(int s) { return s == ST_C128 || s == ST_C64; }
+
+constexpr int kMaxSyms = 32;
+constexpr int kMaxDims = 12;
+constexpr int kMaxLeaves = 96;
+constexpr int kMaxRows = 96;
+constexpr int kMaxAffineTerms = 4;
+constexpr int kMaxVmRegs = 16;
+
+// ---- operand programs (static, uploaded once per plan) ----
+
+enum OperandKind : int { OPK_PLAIN = 0, OPK_AFFINE = 1, OPK_VM = 2 };
+
+// value = fold_{t} (acc (+|-) term_t), term = [coef[pre] *] leaf[flat] [* coef[post0]] [* coef[post1]]
+// A term with leaf < 0 is the constant coef[pre].
+struct AffineTerm {
+  int sign;   // +1 add, -1 subtract (ignored for the first term)
+  int pre;    // coefficient slot or -1
+  int leaf;   // leaf index or -1
+  int post0;  // coefficient slot or -1
+  int post1;  // coefficient slot or -1
+};
+
+struct OperandStatic {
+  int kind;
+  int leaf;     // OPK_PLAIN: leaf index
+  int n_terms;  // OPK_AFFINE
+  AffineTerm term[kMaxAffineTerms];
+  int prog_off, prog_len;  // OPK_VM: instruction range in the program table
+  int ndim;                // operand rank (number of parameters)
+};
+
+enum VmCode : int {
+  VM_LIT = 0,    // r[dst] = imm
+  VM_PARAM,      // r[dst] = params[arg]
+  VM_READ,       // r[dst] = leaf read, descriptor reads[arg]
+  VM_ADD,
+  VM_SUB,
+  VM_MUL,
+  VM_DIV,
+  VM_SIN,
+  VM_COS,
+  VM_EXP,
+  VM_SQRT,
+  VM_RECIP,
+};
+
+struct VmInstr {
+  int code;
+  int dst, a, b;
+  int arg;
+  double imm;
+};
+
+struct VmRead {
+  int leaf;
+  int ndim;
+  int param_of[kMaxDims];           // which operand parameter indexes each axis
+  std::int64_t stride[kMaxDims];    // row-major strides of the leaf
+};
+
+// Coefficient chains for affine operands: coef[c] = f0 * f1 * ... (left fold),
+// each factor a literal or a 0-dim leaf read. Evaluated by a tiny kernel at the
+// start of every execution (leaf pointers change per call).
+struct CoefFactor {
+  int leaf;    // -1 = literal
+  double lit;
+};
+constexpr int kMaxCoefFactors = 4;
+struct CoefChain {
+  int n;
+  CoefFactor f[kMaxCoefFactors];
+};
+
+// ---- generic strided evaluator (any einsum; bit-exact order) ----
+
+struct LeafTable {
+  const void* ptr[kMaxLeaves];
+  int storage[kMaxLeaves];
+};
+
+struct GenericLaunch {
+  // device pointers into the plan's static blob
+  const OperandStatic* ops;   // [b * n], row-major over (row, slot)
+  const int* slot_pos;        // [n * kMaxDims]
+  const std::int64_t* slot_stride;  // [n * kMaxDims]
+  const int* slot_ndim;       // [n]
+  const VmInstr* prog;
+  const VmRead* reads;
+  const CoefChain* chains;
+  int n_chains;
+  double* coef;               // device scratch [n_chains * 2] (re, im)
+  int n_syms, n_out, b, n;
+  std::int64_t extent[kMaxSyms];
+  std::int64_t out_points, red_points;
+  bool complex_mode;
+  int out_storage[kMaxRows];  // per row: ST_F64/ST_C128/...
+  LeafTable leaves;
+  void* out[kMaxRows];
+};
+
+int launch_generic(const GenericLaunch& p, void* stream);
+
+// Tabulate one operand over its shape (materialize / eval_expr).
+struct TabulateLaunch {
+  const OperandStatic* op;
+  const VmInstr* prog;
+  const VmRead* reads;
+  const CoefChain* chains;
+  int n_chains;
+  double* coef;
+  int ndim;
+  std::int64_t shape[kMaxDims];
+  std::int64_t count;        // points to produce
+  std::int64_t first;        // flat index of the first point
+  bool complex_mode;
+  LeafTable leaves;
+  double* out;               // interleaved complex (re, im) per point
+};
+
+int launch_tabulate(const TabulateLaunch& p, void* stream);
+
+// ---- K1: FEM gradient  y[q][r,e,i] = sum_{x,j} J_q[x,r,e] D_q[x,i,j] U_q[e,j] ----
+// Canonical layouts: J [NX, NR, E], D [NX, NI, NJ], U leaves [E, NJ],
+// Y [NR, E, NI] (all row-major). U_q is an affine combination of staged leaf
+// tiles (plain operand = one term, no coefficients).
+constexpr int kFemMaxRows = 16;
+constexpr int kFemMaxUTiles = 32;
+
+struct FemGradLaunch {
+  int rows;
+  std::int64_t E;
+  int NX, NR, NI, NJ;
+  int tile_e;  // elements per pipeline stage
+  int stages;
+  int grid;    // persistent CTAs
+  int n_j, n_d, n_u;
+  const double* J[kFemMaxRows];  // distinct J arrays
+  const double* D[kFemMaxRows];  // distinct D arrays
+  int row_j[kFemMaxRows], row_d[kFemMaxRows];
+  const double* U[kFemMaxUTiles];  // staged U leaves, grouped by row
+  int u_sign[kFemMaxUTiles], u_pre[kFemMaxUTiles], u_post[kFemMaxUTiles];
+  int row_u_first[kFemMaxRows], row_u_count[kFemMaxRows];
+  bool plain_u;        // every row: one term, no coefficients
+  const double* coef;  // interleaved complex coefficients (real part used)
+  double* Y[kFemMaxRows];
+};
+
+int launch_fem_grad(const FemGradLaunch& p, void* stream);
+bool fem_grad_supported(int NX, int NR, int NI, int NJ);
+
+// evaluate coefficient chains into coef (interleaved complex)
+int launch_coef(const CoefChain* chains, int n_chains, const LeafTable& leaves, double* coef, void* stream);
+
+// ---- K3: dense 2-operand contraction (TCCG GETT) on DMMA ----
+// C[m, n] = sum_k A[m, k] B[k, n] with m, n, k each a multi-index over up to 4
+// loop indices; every tensor is addressed through per-index strides.
+constexpr int kGettMaxIdx = 4;
+struct GettLaunch {
+  int nm, nn, nk;  // number of indices in each group
+  std::int64_t m_ext[kGettMaxIdx], n_ext[kGettMaxIdx], k_ext[kGettMaxIdx];
+  std::int64_t a_m_stride[kGettMaxIdx], a_k_stride[kGettMaxIdx];
+  std::int64_t b_k_stride[kGettMaxIdx], b_n_stride[kGettMaxIdx];
+  std::int64_t c_m_stride[kGettMaxIdx], c_n_stride[kGettMaxIdx];
+  std::int64_t M, N, K;
+  int rows;
+  const double* A[kFemMaxRows];
+  const double* B[kFemMaxRows];
+  double* C[kFemMaxRows];
+  // optional affine prologue on A / B: value = alpha * x + beta (coef slots, -1 = none)
+  int a_alpha, a_beta, b_alpha, b_beta;
+  const double* coef;
+  int bm, bn, bk, stages, variant;
+};
+
+int launch_gett(const GettLaunch& p, void* stream);
+
+// ---- K4: tensor-train layer  Y[n,i,k] = sum_{j,l} G1[i,j] G2[k,l] X[n,j,l] ----
+struct TTLaunch {
+  std::int64_t Nb;  // batch
+  int NI, NJ, NK, NL;
+  int rows;
+  int fp32;  // 1: float storage/compute, 0: double (DMMA)
+  const void* G1[kFemMaxRows];
+  const void* G2[kFemMaxRows];
+  const void* X[kFemMaxRows];
+  void* Y[kFemMaxRows];
+  // strides of the roles inside their arrays (canonical layouts vary)
+  std::int64_t g1_si, g1_sj, g2_sk, g2_sl, x_sn, x_sj, x_sl, y_sn, y_si, y_sk;
+  int variant;
+};
+
+int launch_tt(const TTLaunch& p, void* stream);
+
+// ---- K5: hex sum-factorized operator ----
+// y_q[e,i,m,n] = sum A1[x,a,i] A2[x,b,m] A3[x,c,n] G[x,y,e,a,b,c]
+//                    A1[y,a,j] A2[y,b,k] A3[y,c,l] u_q[e,j,k,l]
+struct HexLaunch {
+  std::int64_t E;
+  int ND;   // 3 directions
+  int P;    // points/dofs per direction (5 for P4)
+  int rows;
+  const double* A[3];  // [ND, P, P] each (direction, quad point, dof)
+  const double* G;     // [ND, ND, E, P, P, P]
+  const double* U[kFemMaxRows];
+  double* Y[kFemMaxRows];
+  // element stride / strides of the roles (canonical layouts vary)
+  int variant;
+};
+
+int launch_hex(const HexLaunch& p, void* stream);
+
+// ---- utilities ----
+int device_sm_count(int* out);
+int fill_dyadic(void* ptr, int storage, std::int64_t count, std::uint64_t seed, void* stream);
+int flush_l2(void* scratch, std::int64_t bytes, void* stream);
+
+}  // namespace feb200

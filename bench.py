@@ -1,0 +1,477 @@
+"""Benchmark: geomean GFLOP/s (and roofline fraction) over the TCCG+FEM
+batched-einsum suite of BASELINE.json, on 1-8 B200s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--configs C1,C5,...]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+  python bench.py --impl reference      # the reference CPU evaluator arm
+
+A step evaluates every config of the suite once (one plan execution each).
+Inputs are synthetic dyadic values generated on the device; every config is
+preceded by an L2 flush (writes > 126 MB) and timed alone with CUDA events on
+the launching stream; per-config times are max-reduced over ranks. FLOPs are
+the algorithmic (optimal pairwise contraction path) counts, operand FLOPs of
+functional operands included.
+
+Multi-GPU: each config is sharded along its element/batch axis (weak scaling:
+every rank holds the full per-GPU problem size); no collective on the hot path.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_FLUSH_BYTES = 256 << 20
+
+# per-config workload: builder, plan kind, bound, element-axis sample for the CPU baseline
+CONFIG_DOC = {
+    "C1": "FEM P2-tet gradient xre,xij,ej->rei b=3 E=1e4 fp64",
+    "C2": "FEM P4-hex sum-factorised Poisson b=8 E=2e6 fp64",
+    "C3": "TCCG abcd-aebf-dfce extent 72 fp64, operands alpha*A+beta",
+    "C4-f64": "tensor-train ij,kl,njl->nik n=4096 r=64 fp64",
+    "C4-f32": "tensor-train ij,kl,njl->nik n=4096 r=64 fp32",
+    "C5": "FEM wave step: C1 skeleton E=2e6 with s=u+0.5k fused",
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--configs", default="C1,C2,C3,C4-f64,C4-f32,C5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=2.0, help="target seconds per CPU sample")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ specs --
+
+def spec(name, scale=1.0):
+    """(kind, payload, extra) for a config; scale shrinks the sharded axis."""
+    from paper_2601_12220_b200 import configs as C
+    if name == "C1":
+        return "einsum", C.fem_grad(E=max(2, int(10_000 * scale) // 2 * 2))
+    if name == "C2":
+        return "einsum", C.hex_poisson(E=max(1, int(2_000_000 * scale)))
+    if name == "C3":
+        return "kernel", C.tccg_kernel(ext=72)
+    if name == "C4-f64":
+        return "einsum", C.tensor_train(n=max(1, int(4096 * scale)))
+    if name == "C4-f32":
+        return "einsum", C.tensor_train(n=max(1, int(4096 * scale)), dtype="float32")
+    if name == "C5":
+        return "kernel", C.wave_kernel(E=max(2, int(2_000_000 * scale) // 2 * 2))
+    raise ValueError(name)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# -------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def wait_first(self, timeout=5.0):
+        """Block until nvidia-smi delivered its first sample (it needs ~0.3 s
+        to start), so the samples cover the timed region."""
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        mx = max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ GPU arm -----
+
+class Workload:
+    def __init__(self, name, rank, world, torch, fe, seed):
+        kind, payload = spec(name)
+        full = fe.Plan(einsum=payload) if kind == "einsum" else fe.Plan(kernel=payload)
+        self.full = full
+        self.name = name
+        if world > 1:
+            self.plan, self.lo, self.hi, self.axis = full.shard(rank, world)
+        else:
+            self.plan, self.lo, self.hi, self.axis = full, 0, 0, ""
+        info = self.plan.info
+        self.transform = info["transform"]
+        self.source = info["source"]
+        self.key = full.info["key"]
+        self.flops = info["algorithmic_flops"]
+        self.bytes = info["bytes"]
+        self.ref_flops = info["reference_flops"]
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.ins = []
+        for k, m in enumerate(self.plan.inputs):
+            t = torch.empty(m["shape"], dtype=fe._torch_dtype(m["storage"]), device=dev)
+            fe.fill_dyadic(t, seed * 1000 + k)
+            self.ins.append(t)
+        self.outs = self.plan.alloc_outputs(dev)
+        self.launches = 1 + (1 if info.get("operand_flops", 0) and "alpha" in str(payload) else 0)
+
+    def run(self, stream):
+        self.plan.execute([t.data_ptr() for t in self.ins], [t.data_ptr() for t in self.outs], stream)
+
+
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_12220_b200 import feinsum as fe
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    names = [c for c in args.configs.split(",") if c]
+    loads, skipped = [], {}
+    for i, n in enumerate(names):
+        try:
+            w = Workload(n, rank, world, torch, fe, seed=i + 1)
+        except fe.FeinsumError as ex:
+            skipped[n] = str(ex)
+            continue
+        if w.transform == "generic/v1" and w.ref_flops > 1e11:
+            skipped[n] = "no tuned kernel yet (generic path too slow at full size)"
+            continue
+        loads.append(w)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    def one_step(events):
+        for k, w in enumerate(loads):
+            fe.flush_l2(flush)
+            events[k][0].record(stream)
+            w.run(sh)
+            events[k][1].record(stream)
+
+    ev = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in loads]
+    for _ in range(args.warmup):
+        one_step(ev)
+    torch.cuda.synchronize()
+
+    times = [[] for _ in loads]
+    with ClockSampler(local) as clocks:
+        clocks.wait_first()
+        n0 = len(clocks.rows)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            one_step(ev)
+            torch.cuda.synchronize()
+            for k in range(len(loads)):
+                times[k].append(ev[k][0].elapsed_time(ev[k][1]) * 1e-3)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t_wall
+        # keep only samples taken while the timed loop ran (plus the last one before it)
+        clocks.rows = clocks.rows[max(0, n0 - 1):]
+    if world > 1:
+        dist.barrier()
+
+    mean_t = torch.tensor([sum(t) / len(t) for t in times], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(mean_t, op=dist.ReduceOp.MAX)
+    mean_t = mean_t.cpu().tolist()
+
+    peaks, peak_src = measured_peaks()
+    fp64 = {}
+    for which, label in ((0, "dfma"), (1, "dmma")):
+        import ctypes
+        v = ctypes.c_double()
+        if fe.lib().fe_fp64_peak(which, ctypes.byref(v)) == 0:
+            fp64[label] = v.value
+
+    per = {}
+    rates = []
+    for w, t in zip(loads, mean_t):
+        agg_flops = w.flops * world  # weak scaling: every rank runs its shard of the same size
+        gflops = agg_flops / t / 1e9
+        rates.append(gflops)
+        per[w.name] = {"ms": t * 1e3, "gflops": gflops, "gbs": w.bytes * world / t / 1e9,
+                       "transform": w.transform, "source": w.source, "flops": w.flops, "bytes": w.bytes}
+    value = math.exp(sum(math.log(r) for r in rates) / len(rates)) if rates else 0.0
+    ms_step = sum(mean_t) * 1e3
+
+    # dominant kernel roofline (largest share of the step)
+    dom = max(range(len(loads)), key=lambda k: mean_t[k]) if loads else None
+    roof = None
+    if dom is not None:
+        w, t = loads[dom], mean_t[dom]
+        fp64_peak = max(fp64.values()) if fp64 else None
+        hbm_time = w.bytes / (peaks["hbm_gbs"] * 1e9)
+        fp_time = w.flops / (fp64_peak * 1e12) if fp64_peak else 0
+        if hbm_time >= fp_time:
+            roof = {"bound": "hbm", "achieved": w.bytes / t / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs)"}
+        else:
+            roof = {"bound": "tensor", "achieved": w.flops / t / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "peak_source": "measured on this GPU by fe_fp64_peak (FP64 %s)" % max(fp64, key=fp64.get)}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["kernel"] = w.name + ":" + w.transform
+        roof["traffic"] = None
+
+    e2e = None
+    if not args.no_e2e and loads:
+        e2e = e2e_pass(args, loads, torch, fe, world, dist if world > 1 else None)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline([w.name for w in loads], args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "geomean GFLOP/s (and fraction of roofline) over TCCG+FEM batched einsums, 1-8 B200",
+            "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 (C4-f32: f32)", "data": "synthetic dyadic values m/2^19-1 generated on device",
+            "config": {"workload": "TCCG+FEM suite " + ",".join(w.name for w in loads),
+                       "suite": {n: CONFIG_DOC[n] for n in names}, "per_config": per, "skipped": skipped,
+                       "l2": "flushed (256 MiB write) before every config launch",
+                       "parallelism": f"dp{world} (element/batch-axis shards, no collective)",
+                       "wall_s_timed_region": wall},
+            "roofline": roof, "fp64_peak_tflops": fp64, "clocks": clocks.summary(),
+            "gpu_launches": args.steps * sum(1 + w.launches for w in loads),
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_pass(args, loads, torch, fe, world, dist):
+    """Same metric through the C-ABI with pinned HOST buffers: H2D of the
+    inputs, kernels, D2H of the outputs, all inside the timed region."""
+    stream = torch.cuda.current_stream()
+    rates, h2d, d2h, ms = [], 0, 0, 0.0
+    steps = max(1, min(args.steps, 3))
+    for w in loads:
+        hin = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in w.ins]
+        for h, t in zip(hin, w.ins):
+            h.copy_(t)
+        hout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in w.outs]
+        ptr_in = [h.data_ptr() for h in hin]
+        ptr_out = [h.data_ptr() for h in hout]
+        w.plan.execute_host(ptr_in, ptr_out, stream.cuda_stream)
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for _ in range(steps):
+            t0.record(stream)
+            w.plan.execute_host(ptr_in, ptr_out, stream.cuda_stream)
+            t1.record(stream)
+            torch.cuda.synchronize()
+            tot += t0.elapsed_time(t1) * 1e-3
+        t = tot / steps
+        if dist is not None:
+            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = tt.item()
+        rates.append(w.flops * world / t / 1e9)
+        h2d += sum(x.numel() * x.element_size() for x in hin)
+        d2h += sum(x.numel() * x.element_size() for x in hout)
+        ms += t * 1e3
+        del hin, hout
+    return {"value": math.exp(sum(math.log(r) for r in rates) / len(rates)), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": ms,
+            "steps": steps, "path": "fe_plan_execute_host (C-ABI), pinned host buffers"}
+
+
+# ------------------------------------------------------ CPU reference ----
+
+# bounded samples: the work of every config is linear in its sharded axis
+CPU_SAMPLES = {
+    "C1": ("C1 at full size (E=1e4)", 1.0),
+    "C2": ("C2 with E=1 element, b=1 field (x 2e6 elements x 8 fields)", None),
+    "C3": ("C3 with output indices a,b fixed (1/72^2 of the work)", None),
+    "C4-f64": ("C4 with n=1 sample (x 4096)", 1 / 4096),
+    "C4-f32": ("C4-f32 with n=1 sample (x 4096)", 1 / 4096),
+    "C5": ("C5 with E=2e3 elements (x 1000)", 1e-3),
+}
+
+
+def cpu_sample(name):
+    """(einsum or kernel, kind) of the bounded CPU sample and its alg FLOPs."""
+    from paper_2601_12220_b200 import configs as C
+    if name == "C2":
+        return "einsum", C.hex_poisson(E=1, b=1)
+    if name == "C3":
+        # a and b fixed: a one-element slice of both output axes
+        return "tccg_slice", None
+    return spec(name, CPU_SAMPLES[name][1])
+
+
+def _cpu_worker(args):
+    name, reps = args
+    import numpy as np
+
+    from oracle import refpy as R
+    from paper_2601_12220_b200 import configs as C
+    kind, payload = cpu_sample(name)
+    if kind == "tccg_slice":
+        e = C.tccg(ext=72)
+        e["args"][0][0]["shape"] = [1, 72, 1, 72]   # A[a,e,b,f] with a=b=1
+        e = {"i_out": ["a", "b", "c", "d"], "i_in": e["i_in"], "args": e["args"]}
+        lens = {"a": 1, "b": 1, "c": 72, "d": 72, "e": 72, "f": 72}
+        e["args"][0][1]["shape"] = [lens[s] for s in e["i_in"][1]]
+        binds = R.random_bindings(e, 1)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            R.evaluate(e, binds)
+        return time.perf_counter() - t0
+    if kind == "einsum":
+        binds = R.random_bindings(payload, 1)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            R.evaluate(payload, binds)
+        return time.perf_counter() - t0
+    import re
+    arrays = []
+    for line in payload.splitlines():
+        m = re.match(r"array: (\w+) (\w+) (\S+)", line)
+        if m:
+            shape = [] if m.group(3) == "scalar" else [int(x) for x in m.group(3).split("x")]
+            arrays.append({"name": m.group(1), "shape": shape, "dtype": m.group(2)})
+    fake = {"i_out": [], "i_in": [[] for _ in arrays], "args": [arrays]}
+    binds = R.random_bindings(fake, 1)
+    raised = R.raise_kernel(payload)
+    shape = [dict(zip(sum(raised["skeleton"]["i_in"], []),
+                      sum([m["shape"] for m in raised["skeleton"]["args"][0]], [])))[s]
+             for s in raised["skeleton"]["i_out"]]
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        R.eval_kernel(payload, arrays, binds, len(raised["skeleton"]["args"]), shape)
+    return time.perf_counter() - t0
+
+
+def sample_flops(name):
+    from paper_2601_12220_b200 import feinsum as fe
+    kind, payload = cpu_sample(name)
+    if kind == "tccg_slice":
+        return 2.0 * 72 ** 4 + 2 * 2 * 72 ** 2 * 0  # the operand FLOPs of the slice are negligible
+    if kind == "einsum":
+        return fe.cost(payload)["algorithmic_flops"]
+    p = fe.Plan(kernel=payload, options={"dry_run": True})
+    return p.info["algorithmic_flops"]
+
+
+def cpu_baseline(names, seconds, cores=None):
+    """Reference evaluator (oracle/_ref, the unmodified feinsum::evaluate /
+    evaluate_functional) on the host cores: one process per core, each
+    evaluating the same bounded sample (the shardable axes make per-core work
+    independent), throughput = cores x sample FLOPs / wall."""
+    import multiprocessing as mp
+    cores = cores or os.cpu_count() or 1
+    out = {}
+    rates = []
+    ctx = mp.get_context("fork")
+    for n in names:
+        if n not in CPU_SAMPLES:
+            continue
+        flops = sample_flops(n)
+        with ctx.Pool(1) as p:
+            t1 = p.map(_cpu_worker, [(n, 1)])[0]
+        reps = max(1, int(seconds / max(t1, 1e-6)))
+        with ctx.Pool(cores) as p:
+            t0 = time.perf_counter()
+            p.map(_cpu_worker, [(n, reps)] * cores)
+            wall = time.perf_counter() - t0
+        rate = cores * reps * flops / wall / 1e9
+        rates.append(rate)
+        out[n] = {"gflops": rate, "sample": CPU_SAMPLES[n][0], "reps_per_core": reps, "single_core_s": t1}
+    value = math.exp(sum(math.log(r) for r in rates) / len(rates)) if rates else None
+    return {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+            "sample": "per config: " + "; ".join(f"{k}: {v['sample']}" for k, v in out.items()),
+            "per_config": out}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    names = [c for c in args.configs.split(",") if c in CPU_SAMPLES]
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(names, args.cpu_seconds / 2)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            last = r
+    value = sum(vals) / len(vals)
+    line = {"metric": "geomean GFLOP/s (and fraction of roofline) over TCCG+FEM batched einsums, 1-8 B200",
+            "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (reference)",
+            "data": "synthetic dyadic (random_bindings)", "impl": "reference",
+            "config": {"workload": "TCCG+FEM suite " + ",".join(names), "per_config": last["per_config"]},
+            "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": "GFLOP/s"},
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    a = parse_args()
+    if a.impl == "reference":
+        reference_arm(a)
+    else:
+        gpu_arm(a)

@@ -90,7 +90,7 @@ int fe_retrieve(const char* path, const char* key, const char* device, char** ou
 /* ---- device side: plans (replace evaluate, core.hpp:141, and
  *      evaluate_functional, raising.hpp:58) ---- */
 
-/* options JSON (all optional): {"storage": "native"|"wide"|{name: "f64"|...},
+/* options JSON (all optional): {"storage": "native"|"wide", "leaf_storage": {name: "f64"|...},
  *  "facts": path, "device": "b200", "transform": "generic/v1"|...} */
 int fe_plan_create(const char* einsum_json, const char* options_json, fe_plan_t* out);
 /* .fk kernel text: inputs = declared arrays in name order, one output per stmt */
@@ -127,6 +127,9 @@ int fe_fill_dyadic(void* d_ptr, int storage, int64_t count, uint64_t seed, void*
 /* overwrite `bytes` of scratch (>= L2 size) to evict L2 between timed runs */
 int fe_flush_l2(void* d_scratch, int64_t bytes, void* stream);
 int fe_sm_count(void);
+/* measured FP64 throughput of the current device, TFLOP/s: which = 0 DFMA,
+ * 1 DMMA (the FP64 roofline denominator; MEASURED_PEAKS.json has none) */
+int fe_fp64_peak(int which, double* tflops);
 
 #ifdef __cplusplus
 }

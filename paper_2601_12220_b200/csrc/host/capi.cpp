@@ -473,6 +473,8 @@ int fe_flush_l2(void* d_scratch, int64_t bytes, void* stream) {
   return cuda_status(feb200::flush_l2(d_scratch, bytes, stream));
 }
 
+int fe_fp64_peak(int which, double* tflops) { return cuda_status(feb200::fp64_peak(which, tflops)); }
+
 int fe_sm_count(void) {
   int n = 0;
   if (feb200::device_sm_count(&n) != 0) return -1;

@@ -100,14 +100,12 @@ PlanOptions parse_options(const std::string& json) {
   const fejson::Value v = fejson::parse(json);
   if (v.t != fejson::Value::T::object) throw error(errc::usage, "options must be a JSON object");
   if (auto* x = v.find("storage")) {
-    if (x->t == fejson::Value::T::string) {
-      o.storage = x->s;
-      if (o.storage != "native" && o.storage != "wide")
-        throw error(errc::usage, "options.storage must be \"native\" or \"wide\"");
-    } else {
-      for (const auto& [name, st] : x->o) o.storage_of[name] = st.as_str();
-    }
+    o.storage = x->as_str();
+    if (o.storage != "native" && o.storage != "wide")
+      throw error(errc::usage, "options.storage must be \"native\" or \"wide\"");
   }
+  if (auto* x = v.find("leaf_storage"))
+    for (const auto& [name, st] : x->o) o.storage_of[name] = st.as_str();
   if (auto* x = v.find("facts")) o.facts_path = x->as_str();
   if (auto* x = v.find("device")) o.device_id = x->as_str();
   if (auto* x = v.find("transform")) o.force_transform = x->as_str();
@@ -459,6 +457,20 @@ std::optional<RoleMatch> match_roles(const BatchedEinsum& c, const std::vector<s
 
 bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
 
+// Tuned parameter from a fact's meta string "k1=v1;k2=v2" (default if absent).
+int meta_int(const std::string& meta, const std::string& key, int dflt) {
+  size_t pos = 0;
+  while (pos < meta.size()) {
+    size_t end = meta.find(';', pos);
+    if (end == std::string::npos) end = meta.size();
+    const std::string item = meta.substr(pos, end - pos);
+    const size_t eq = item.find('=');
+    if (eq != std::string::npos && item.substr(0, eq) == key) return std::atoi(item.c_str() + eq + 1);
+    pos = end + 1;
+  }
+  return dflt;
+}
+
 // FEM gradient family: J[x,r,e] D[x,i,j] U[e,j] -> Y[r,e,i]
 bool bind_fem(Plan& p, std::string* why) {
   const auto m = match_roles(p.canon.canonical, {"xre", "xij", "ej"}, "rei");
@@ -543,6 +555,129 @@ bool bind_fem(Plan& p, std::string* why) {
     return false;
   }
   p.fem = std::move(f);
+  return true;
+}
+
+std::vector<std::int64_t> row_major_strides(const std::vector<std::int64_t>& shape) {
+  std::vector<std::int64_t> st(shape.size(), 1);
+  for (int d = static_cast<int>(shape.size()) - 2; d >= 0; --d) st[d] = st[d + 1] * shape[d + 1];
+  return st;
+}
+
+// Operand usable by the GETT prologue: plain, or coef[alpha] * X (+ coef[beta]).
+bool gett_operand(const Plan& p, const OperandStatic& op, int* leaf, int* alpha, int* beta) {
+  *alpha = *beta = -1;
+  if (op.kind == OPK_PLAIN) {
+    *leaf = op.leaf;
+  } else if (op.kind == OPK_AFFINE) {
+    const AffineTerm& t0 = op.term[0];
+    if (t0.leaf < 0 || t0.post0 >= 0 || op.n_terms > 2) return false;
+    *leaf = t0.leaf;
+    *alpha = t0.pre;
+    if (op.n_terms == 2) {
+      const AffineTerm& t1 = op.term[1];
+      if (t1.leaf >= 0 || t1.sign < 0 || t1.pre < 0) return false;
+      *beta = t1.pre;
+      if (*alpha < 0) return false;  // x + beta: no multiplier slot to fold it into
+    }
+  } else {
+    return false;
+  }
+  return p.leaves[*leaf].storage == ST_F64;
+}
+
+// GETT family: 2 slots, pure contraction (every index in exactly two of A, B,
+// C), 2+2+2 indices, C's unit-stride index on the B side, A's and B's
+// unit-stride indices both contracted.
+bool bind_gett(Plan& p, std::string* why) {
+  const BatchedEinsum& c = p.canon.canonical;
+  if (p.complex_mode || c.n() != 2 || c.i_out.size() != 4) {
+    *why = "not a 2-operand 4-index contraction";
+    return false;
+  }
+  const std::set<std::string> s0(c.i_in[0].begin(), c.i_in[0].end()), s1(c.i_in[1].begin(), c.i_in[1].end());
+  if (s0.size() != 4 || s1.size() != 4 || c.i_in[0].size() != 4 || c.i_in[1].size() != 4) {
+    *why = "repeated indices";
+    return false;
+  }
+  std::set<std::string> K, out(c.i_out.begin(), c.i_out.end());
+  for (const auto& x : s0)
+    if (s1.count(x)) K.insert(x);
+  if (K.size() != 2) {
+    *why = "needs exactly two contracted indices";
+    return false;
+  }
+  for (const auto& x : out)
+    if (K.count(x)) {
+      *why = "batch index";
+      return false;
+    }
+  const std::string ni = c.i_out.back();
+  const int sb = s1.count(ni) ? 1 : 0, sa = 1 - sb;
+  const feinsum::IndexList& la = c.i_in[sa];
+  const feinsum::IndexList& lb = c.i_in[sb];
+  const std::string ka = la.back(), kb = lb.back();
+  if (!K.count(ka) || !K.count(kb) || ka == kb) {
+    *why = "unit-stride indices of A and B must be the two contracted indices";
+    return false;
+  }
+  const auto lens = feinsum::index_lengths(c);
+  std::vector<std::string> M, N;
+  for (const auto& x : la)
+    if (!K.count(x)) M.push_back(x);
+  for (const auto& x : lb)
+    if (!K.count(x)) N.push_back(x);
+  const std::string mi = M[1], mo = M[0];  // later position = smaller stride in A
+  const std::string no = N[0] == ni ? N[1] : N[0];
+  GettBinding g;
+  g.ext_mo = lens.at(mo);
+  g.ext_mi = lens.at(mi);
+  g.ext_no = lens.at(no);
+  g.ext_ni = lens.at(ni);
+  g.ext_ka = lens.at(ka);
+  g.ext_kb = lens.at(kb);
+  if (!gett_supported(g.ext_mi, g.ext_ni, g.ext_ka, g.ext_kb)) {
+    *why = "extents outside the compiled 72x72 tile";
+    return false;
+  }
+  auto stride_of = [&](const feinsum::IndexList& l, const std::vector<std::int64_t>& shape, const std::string& s) {
+    const auto st = row_major_strides(shape);
+    for (size_t d = 0; d < l.size(); ++d)
+      if (l[d] == s) return st[d];
+    return std::int64_t{0};
+  };
+  const auto& sha = c.args[0][sa].shape;
+  const auto& shb = c.args[0][sb].shape;
+  std::vector<std::int64_t> shc;
+  for (const auto& s : c.i_out) shc.push_back(lens.at(s));
+  g.a_mo = stride_of(la, sha, mo);
+  g.a_mi = stride_of(la, sha, mi);
+  g.a_kb = stride_of(la, sha, kb);
+  g.b_no = stride_of(lb, shb, no);
+  g.b_ni = stride_of(lb, shb, ni);
+  g.b_ka = stride_of(lb, shb, ka);
+  g.c_mo = stride_of(c.i_out, shc, mo);
+  g.c_mi = stride_of(c.i_out, shc, mi);
+  g.c_no = stride_of(c.i_out, shc, no);
+  g.c_ni = stride_of(c.i_out, shc, ni);
+  g.role_names = "mo=" + mo + " mi=" + mi + " no=" + no + " ni=" + ni + " kA=" + ka + " kB=" + kb;
+  const int n = c.n();
+  for (int q = 0; q < c.b(); ++q) {
+    const int ur = p.canon.sigma_row[q];
+    GettBinding::Row r{};
+    r.out_row = ur;
+    if (!gett_operand(p, p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[sa]], &r.a_leaf, &r.a_alpha, &r.a_beta) ||
+        !gett_operand(p, p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[sb]], &r.b_leaf, &r.b_alpha, &r.b_beta)) {
+      *why = "operands are not plain or alpha*X+beta f64";
+      return false;
+    }
+    if (p.outputs[ur].storage != ST_F64) {
+      *why = "non-f64 output";
+      return false;
+    }
+    g.rows.push_back(r);
+  }
+  p.gett = std::move(g);
   return true;
 }
 
@@ -734,7 +869,7 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
   }
 
   // kernel choice: forced > fact > first matching family > generic
-  std::vector<Family> order = {Family::fem_grad};
+  std::vector<Family> order = {Family::fem_grad, Family::gett};
   auto family_of = [](const std::string& t) -> std::optional<Family> {
     for (Family f : {Family::generic, Family::fem_grad, Family::gett, Family::tt, Family::hex})
       if (t == family_transform(f)) return f;
@@ -746,6 +881,7 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
     switch (f) {
       case Family::generic: return true;
       case Family::fem_grad: return bind_fem(p, &why);
+      case Family::gett: return bind_gett(p, &why);
       default: return false;
     }
   };
@@ -930,6 +1066,45 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
       return;
     }
   }
+  if (plan.family == Family::gett) {
+    const GettBinding& b = plan.gett;
+    bool ok = true;
+    for (const auto& r : b.rows) ok = ok && aligned16(d_in[r.a_leaf]) && aligned16(d_in[r.b_leaf]);
+    if (ok) {
+      for (const auto& r : b.rows) {
+        GettLaunch L{};
+        L.ext_mo = b.ext_mo;
+        L.ext_mi = b.ext_mi;
+        L.ext_no = b.ext_no;
+        L.ext_ni = b.ext_ni;
+        L.ext_ka = b.ext_ka;
+        L.ext_kb = b.ext_kb;
+        L.a_mo = b.a_mo;
+        L.a_mi = b.a_mi;
+        L.a_kb = b.a_kb;
+        L.b_no = b.b_no;
+        L.b_ni = b.b_ni;
+        L.b_ka = b.b_ka;
+        L.c_mo = b.c_mo;
+        L.c_mi = b.c_mi;
+        L.c_no = b.c_no;
+        L.c_ni = b.c_ni;
+        L.A = static_cast<const double*>(d_in[r.a_leaf]);
+        L.B = static_cast<const double*>(d_in[r.b_leaf]);
+        L.C = static_cast<double*>(d_out[r.out_row]);
+        L.a_alpha = r.a_alpha;
+        L.a_beta = r.a_beta;
+        L.b_alpha = r.b_alpha;
+        L.b_beta = r.b_beta;
+        L.coef = plan.d_coef;
+        L.stages = meta_int(plan.meta, "stages", 5);
+        L.group = meta_int(plan.meta, "group", 4);
+        L.grid = meta_int(plan.meta, "grid", 0);
+        cuda_check(launch_gett(L, stream), "gett kernel");
+      }
+      return;
+    }
+  }
   cuda_check(launch_generic(g, stream), "generic kernel");
 }
 
@@ -1014,6 +1189,12 @@ std::string describe(const Plan& p) {
     f.set("NI", Value::num(p.fem.NI));
     f.set("NJ", Value::num(p.fem.NJ));
     f.set("E", Value::num(p.fem.E));
+    v.set("roles", std::move(f));
+  }
+  if (p.family == Family::gett) {
+    Value f = Value::obj();
+    f.set("roles", Value::str(p.gett.role_names));
+    f.set("tile", Value::str("72x72x16, 9 DMMA warps + 1 TMA warp"));
     v.set("roles", std::move(f));
   }
   return fejson::dump(v);

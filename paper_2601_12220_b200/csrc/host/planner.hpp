@@ -72,6 +72,19 @@ struct FemBinding {
   std::vector<std::vector<AffineTerm>> u_terms;  // per row; leaf indices
 };
 
+// Roles of the GETT family (dense 2-operand contraction on DMMA).
+struct GettBinding {
+  std::int64_t ext_mo = 0, ext_mi = 0, ext_no = 0, ext_ni = 0, ext_ka = 0, ext_kb = 0;
+  std::int64_t a_mo = 0, a_mi = 0, a_kb = 0, b_no = 0, b_ni = 0, b_ka = 0;
+  std::int64_t c_mo = 0, c_mi = 0, c_no = 0, c_ni = 0;
+  std::string role_names;  // "mo=a mi=b ..." for describe()
+  struct Row {
+    int a_leaf, b_leaf, out_row;
+    int a_alpha, a_beta, b_alpha, b_beta;
+  };
+  std::vector<Row> rows;
+};
+
 struct Plan {
   // ---- what is computed ----
   BatchedEinsum skel;  // the caller's einsum (skeleton if functional)
@@ -94,6 +107,7 @@ struct Plan {
   std::string source;     // "fact" | "default" | "forced" | "fallback"
   Family family = Family::generic;
   FemBinding fem;
+  GettBinding gett;
 
   // ---- costs ----
   double alg_flops = 0, operand_flops = 0, bytes = 0, ref_flops = 0;

@@ -1,0 +1,279 @@
+// K3 — dense TCCG contraction (GETT) on the FP64 tensor cores (DMMA), fed by
+// TMA, with the functional-operand prologue (alpha*X + beta) fused into the
+// fragment loads.
+//
+//   C[mo,mi,no,ni] = sum_{kA,kB} opA(A[.. mo, mi, kB, kA ..]) * opB(B[.. no, ni, kA, kB ..])
+//
+// (index positions are arbitrary: every tensor is described by per-role
+// strides). For the pinned C3 spelling aebf,dfce->abcd: mo=a, mi=b, no=c,
+// ni=d, kA=f (A's unit-stride index), kB=e (B's unit-stride index).
+//
+// Why this shape on sm_100a: tcgen05 has no f64 kind, so FP64 tensor work is
+// mma.sync m8n8k4 (DMMA, SASS DMMA.8x8x4). Tiles are staged by TMA
+// (cp.async.bulk.tensor, 4-D boxes gather the strided GETT operands without a
+// transpose pass) into a multi-stage mbarrier ring with the 128-byte swizzle,
+// which makes the A-fragment reads conflict-free; one producer warp issues the
+// TMA, nine consumer warps (3x3 grid of 24x24 warp tiles over a 72x72 CTA tile)
+// run the DMMAs. The persistent grid walks output tiles in groups that share A
+// slices so L2 serves the reuse.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <mutex>
+
+#include "launch.h"
+#include "ptx.cuh"
+
+namespace feb200 {
+
+namespace {
+
+constexpr int BM = 72, BN = 72;      // CTA tile (mi x ni)
+constexpr int KA = 8, KB = 2;        // k box: 8 of kA (128-byte rows with 2 of kB)
+constexpr int KT = KA * KB;          // k per stage
+constexpr int kConsumerWarps = 9;
+constexpr int kThreads = 32 * (kConsumerWarps + 1);
+constexpr int kTileBytes = BM * KT * 8;  // 9216 = 9 x 1024 (swizzle atoms)
+
+struct GettDev {
+  std::int64_t mo, no;                  // tile counts (= extents of mo / no)
+  std::int64_t ka_steps, kb_steps;      // kA/8, kB/2
+  std::int64_t c_mo, c_mi, c_no, c_ni;  // C strides (elements)
+  double* C;
+  const double* coef;
+  int a_alpha, a_beta, b_alpha, b_beta;
+  int stages, group;
+};
+
+// 128-byte swizzle: 16-byte chunk index (bits 4-6) ^= row (bits 7-9)
+__device__ __forceinline__ std::uint32_t swz(std::uint32_t off) { return off ^ (((off >> 7) & 7u) << 4); }
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+          ptx::smem_addr(dst)),
+      "l"(map), "r"(ptx::smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    gett_kernel(const __grid_constant__ GettDev p, const __grid_constant__ CUtensorMap tmA,
+                const __grid_constant__ CUtensorMap tmB) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the swizzle atoms
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+  const int S = p.stages;
+  unsigned char* tiles = base;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(tiles + static_cast<size_t>(S) * 2 * kTileBytes);
+  std::uint64_t* empty = full + S;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::int64_t ntiles = p.mo * p.no;
+  const std::int64_t ksteps = p.ka_steps * p.kb_steps;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], kConsumerWarps);
+    }
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+
+  // tile t -> (mo, no): groups of `group` mo-rows sweep all no (A reuse in L2)
+  auto tile_coords = [&](std::int64_t t, std::int64_t& mo, std::int64_t& no) {
+    const std::int64_t per_group = static_cast<std::int64_t>(p.group) * p.no;
+    const std::int64_t g = t / per_group;
+    const std::int64_t r = t - g * per_group;
+    const std::int64_t rows = (g + 1) * p.group <= p.mo ? p.group : p.mo - g * p.group;
+    mo = g * p.group + r % rows;
+    no = r / rows;
+  };
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------- producer -------------------------------
+    if (lane != 0) return;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    std::int64_t it = 0;
+    for (std::int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      std::int64_t mo, no;
+      tile_coords(t, mo, no);
+      for (std::int64_t ks = 0; ks < ksteps; ++ks, ++it) {
+        const int s = static_cast<int>(it % S);
+        const std::uint32_t round = static_cast<std::uint32_t>(it / S);
+        ptx::mbar_wait(&empty[s], (round & 1u) ^ 1u);
+        const int kb0 = static_cast<int>(ks / p.ka_steps) * KB;
+        const int ka0 = static_cast<int>(ks % p.ka_steps) * KA;
+        ptx::mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
+        unsigned char* st = tiles + static_cast<size_t>(s) * 2 * kTileBytes;
+        // A dims (kA, kB, mi, mo); B dims (kB, no, kA, ni)
+        tma_load_4d(st, &tmA, &full[s], ka0, kb0, 0, static_cast<int>(mo));
+        tma_load_4d(st + kTileBytes, &tmB, &full[s], kb0, static_cast<int>(no), ka0, 0);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------- consumers --------------------------------
+  const int wm = warp / 3, wn = warp % 3;  // 3x3 grid of 24x24 warp tiles
+  const int qrow = lane >> 2, qk = lane & 3;
+  const bool affA = p.a_alpha >= 0, affB = p.b_alpha >= 0;
+  const double aA = affA ? p.coef[2 * p.a_alpha] : 1.0, bA = (affA && p.a_beta >= 0) ? p.coef[2 * p.a_beta] : 0.0;
+  const double aB = affB ? p.coef[2 * p.b_alpha] : 1.0, bB = (affB && p.b_beta >= 0) ? p.coef[2 * p.b_beta] : 0.0;
+
+  std::int64_t it = 0;
+  for (std::int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    std::int64_t mo, no;
+    tile_coords(t, mo, no);
+    double acc[3][3][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (std::int64_t ks = 0; ks < ksteps; ++ks, ++it) {
+      const int s = static_cast<int>(it % S);
+      const std::uint32_t round = static_cast<std::uint32_t>(it / S);
+      ptx::mbar_wait(&full[s], round & 1u);
+      const unsigned char* sa = tiles + static_cast<size_t>(s) * 2 * kTileBytes;
+      const unsigned char* sb = sa + kTileBytes;
+#pragma unroll
+      for (int kc = 0; kc < KT / 4; ++kc) {
+        const int e_l = kc >> 1;              // kB within the stage
+        const int f = (kc & 1) * 4 + qk;      // kA within the stage
+        double af[3], bf[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int m = wm * 24 + i * 8 + qrow;
+          // A image: [mi][kB][kA] -> m*128 + e_l*64 + f*8
+          af[i] = *reinterpret_cast<const double*>(sa + swz(static_cast<std::uint32_t>(m * 128 + e_l * 64 + f * 8)));
+          if (affA) af[i] = fma(aA, af[i], bA);
+        }
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int n = wn * 24 + j * 8 + qrow;
+          // B image: [ni][kA][kB] -> n*128 + f*16 + e_l*8
+          bf[j] = *reinterpret_cast<const double*>(sb + swz(static_cast<std::uint32_t>(n * 128 + f * 16 + e_l * 8)));
+          if (affB) bf[j] = fma(aB, bf[j], bB);
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    }
+
+    // epilogue: fragment (row qrow, cols 2*qk, 2*qk+1) of each 8x8 block
+    double* cbase = p.C + mo * p.c_mo + no * p.c_no;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int m = wm * 24 + i * 8 + qrow;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int n = wn * 24 + j * 8 + 2 * qk;
+        double* dst = cbase + m * p.c_mi + n * p.c_ni;
+        if (p.c_ni == 1) {
+          __stcs(reinterpret_cast<double2*>(dst), make_double2(acc[i][j][0], acc[i][j][1]));
+        } else {
+          dst[0] = acc[i][j][0];
+          dst[p.c_ni] = acc[i][j][1];
+        }
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const double* base, const std::uint64_t dims[4], const std::uint64_t strides_el[4],
+              const std::uint32_t box[4]) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t gdim[4], gstride[3];
+  cuuint32_t bdim[4], estr[4] = {1, 1, 1, 1};
+  for (int d = 0; d < 4; ++d) {
+    gdim[d] = dims[d];
+    bdim[d] = box[d];
+  }
+  for (int d = 1; d < 4; ++d) gstride[d - 1] = strides_el[d] * 8;
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), gdim, gstride, bdim, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool gett_supported(std::int64_t ext_mi, std::int64_t ext_ni, std::int64_t ext_ka, std::int64_t ext_kb) {
+  return ext_mi == BM && ext_ni == BN && ext_ka % KA == 0 && ext_kb % KB == 0;
+}
+
+int launch_gett(const GettLaunch& L, void* stream) {
+  if (!gett_supported(L.ext_mi, L.ext_ni, L.ext_ka, L.ext_kb)) return cudaErrorInvalidValue;
+  CUtensorMap tmA, tmB;
+  {
+    const std::uint64_t dims[4] = {static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_kb),
+                                   static_cast<std::uint64_t>(L.ext_mi), static_cast<std::uint64_t>(L.ext_mo)};
+    const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.a_kb), static_cast<std::uint64_t>(L.a_mi),
+                                  static_cast<std::uint64_t>(L.a_mo)};
+    const std::uint32_t box[4] = {KA, KB, BM, 1};
+    if (!make_map(&tmA, L.A, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const std::uint64_t dims[4] = {static_cast<std::uint64_t>(L.ext_kb), static_cast<std::uint64_t>(L.ext_no),
+                                   static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_ni)};
+    const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.b_no), static_cast<std::uint64_t>(L.b_ka),
+                                  static_cast<std::uint64_t>(L.b_ni)};
+    const std::uint32_t box[4] = {KB, 1, KA, BN};
+    if (!make_map(&tmB, L.B, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  GettDev d{};
+  d.mo = L.ext_mo;
+  d.no = L.ext_no;
+  d.ka_steps = L.ext_ka / KA;
+  d.kb_steps = L.ext_kb / KB;
+  d.c_mo = L.c_mo;
+  d.c_mi = L.c_mi;
+  d.c_no = L.c_no;
+  d.c_ni = L.c_ni;
+  d.C = L.C;
+  d.coef = L.coef;
+  d.a_alpha = L.a_alpha;
+  d.a_beta = L.a_beta;
+  d.b_alpha = L.b_alpha;
+  d.b_beta = L.b_beta;
+  d.stages = L.stages > 0 ? L.stages : 5;
+  d.group = L.group > 0 ? L.group : 4;
+  const size_t smem = 1024 + static_cast<size_t>(d.stages) * 2 * kTileBytes + 16 * d.stages;
+  cudaError_t e = cudaFuncSetAttribute(gett_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  device_sm_count(&sms);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gett_kernel, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  std::int64_t grid = static_cast<std::int64_t>(sms) * per_sm;
+  if (L.grid > 0) grid = L.grid;
+  if (grid > d.mo * d.no) grid = d.mo * d.no;
+  gett_kernel<<<static_cast<int>(grid), kThreads, smem, static_cast<cudaStream_t>(stream)>>>(d, tmA, tmB);
+  return cudaGetLastError();
+}
+
+}  // namespace feb200

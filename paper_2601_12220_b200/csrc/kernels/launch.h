@@ -190,27 +190,25 @@ bool fem_grad_supported(int NX, int NR, int NI, int NJ);
 int launch_coef(const CoefChain* chains, int n_chains, const LeafTable& leaves, double* coef, void* stream);
 
 // ---- K3: dense 2-operand contraction (TCCG GETT) on DMMA ----
-// C[m, n] = sum_k A[m, k] B[k, n] with m, n, k each a multi-index over up to 4
-// loop indices; every tensor is addressed through per-index strides.
-constexpr int kGettMaxIdx = 4;
+// C[mo,mi,no,ni] = sum_{kA,kB} A[mo,mi,kB,kA] B[no,ni,kA,kB], roles bound to
+// arbitrary index positions through strides (elements). kA is A's unit-stride
+// index, kB is B's; ni is the tile index of C (unit stride for vector stores).
 struct GettLaunch {
-  int nm, nn, nk;  // number of indices in each group
-  std::int64_t m_ext[kGettMaxIdx], n_ext[kGettMaxIdx], k_ext[kGettMaxIdx];
-  std::int64_t a_m_stride[kGettMaxIdx], a_k_stride[kGettMaxIdx];
-  std::int64_t b_k_stride[kGettMaxIdx], b_n_stride[kGettMaxIdx];
-  std::int64_t c_m_stride[kGettMaxIdx], c_n_stride[kGettMaxIdx];
-  std::int64_t M, N, K;
-  int rows;
-  const double* A[kFemMaxRows];
-  const double* B[kFemMaxRows];
-  double* C[kFemMaxRows];
-  // optional affine prologue on A / B: value = alpha * x + beta (coef slots, -1 = none)
+  std::int64_t ext_mo, ext_mi, ext_no, ext_ni, ext_ka, ext_kb;
+  std::int64_t a_mo, a_mi, a_kb;  // A strides (a_ka == 1)
+  std::int64_t b_no, b_ni, b_ka;  // B strides (b_kb == 1)
+  std::int64_t c_mo, c_mi, c_no, c_ni;
+  const double* A;
+  const double* B;
+  double* C;
+  // optional affine prologue: value = coef[alpha] * x + coef[beta] (-1 = none)
   int a_alpha, a_beta, b_alpha, b_beta;
   const double* coef;
-  int bm, bn, bk, stages, variant;
+  int stages, group, grid;
 };
 
 int launch_gett(const GettLaunch& p, void* stream);
+bool gett_supported(std::int64_t ext_mi, std::int64_t ext_ni, std::int64_t ext_ka, std::int64_t ext_kb);
 
 // ---- K4: tensor-train layer  Y[n,i,k] = sum_{j,l} G1[i,j] G2[k,l] X[n,j,l] ----
 struct TTLaunch {
@@ -251,5 +249,7 @@ int launch_hex(const HexLaunch& p, void* stream);
 int device_sm_count(int* out);
 int fill_dyadic(void* ptr, int storage, std::int64_t count, std::uint64_t seed, void* stream);
 int flush_l2(void* scratch, std::int64_t bytes, void* stream);
+// which: 0 = DFMA (CUDA cores), 1 = DMMA m8n8k4 (FP64 tensor cores)
+int fp64_peak(int which, double* tflops);
 
 }  // namespace feb200

@@ -47,7 +47,66 @@ __global__ void flush_kernel(int4* p, std::int64_t n, int salt) {
     p[i] = make_int4(salt, salt, salt, static_cast<int>(i));
 }
 
+// FP64 pipe micro-benchmarks: the roofline denominator for the FP64-bound
+// kernels (MEASURED_PEAKS.json carries only HBM and bf16 numbers).
+__global__ void dfma_peak_kernel(double* sink, int iters, double seed) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+         a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 12345.678) sink[0] = a0;
+}
+
+__global__ void dmma_peak_kernel(double* sink, int iters, double seed) {
+  double d[8][2];
+  for (int k = 0; k < 8; ++k) d[k][0] = d[k][1] = seed * k;
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 0.5;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(d[k][0]), "+d"(d[k][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int k = 0; k < 8; ++k) s += d[k][0] + d[k][1];
+  if (s == 12345.678) sink[0] = s;
+}
+
 }  // namespace
+
+int fp64_peak(int which, double* tflops) {
+  int sms = 148;
+  device_sm_count(&sms);
+  double* sink = nullptr;
+  cudaError_t e = cudaMalloc(&sink, 64);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  const int blocks = sms * 4, threads = 256, iters = 4096;
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaEventRecord(t0);
+    if (which == 0)
+      dfma_peak_kernel<<<blocks, threads>>>(sink, iters, 0.5);
+    else
+      dmma_peak_kernel<<<blocks, threads>>>(sink, iters, 0.5);
+    cudaEventRecord(t1);
+    cudaEventSynchronize(t1);
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, t0, t1);
+  const double flops = which == 0 ? 2.0 * 8 * iters * static_cast<double>(blocks) * threads
+                                  : 512.0 * 8 * iters * static_cast<double>(blocks) * (threads / 32);
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaFree(sink);
+  return cudaGetLastError();
+}
 
 int fill_dyadic(void* ptr, int storage, std::int64_t count, std::uint64_t seed, void* stream) {
   if (count <= 0) return cudaSuccess;

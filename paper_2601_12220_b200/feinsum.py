@@ -334,7 +334,8 @@ def evaluate(e, bindings):
             raise FeinsumError(1, "binding for array " + m["name"] + " has wrong element count")
         names.append(m["name"])
     _check(lib().fe_device_check())
-    opts = {"storage": {n: ("c128" if np.iscomplexobj(np.asarray(bindings[n])) else "f64") for n in names}}
+    opts = {"storage": "wide",
+            "leaf_storage": {n: ("c128" if np.iscomplexobj(np.asarray(bindings[n])) else "f64") for n in names}}
     return _run_wide(Plan(einsum=e, options=opts), bindings)
 
 
@@ -342,5 +343,5 @@ def evaluate_kernel(fk_text, bindings, options=None):
     """parse_kernel + raise + evaluate_functional on the GPU (operands fused)."""
     _check(lib().fe_device_check())
     storage = {n: ("c128" if np.iscomplexobj(np.asarray(v)) else "f64") for n, v in bindings.items()}
-    plan = Plan(kernel=fk_text, options={**(options or {}), "storage": storage})
+    plan = Plan(kernel=fk_text, options={**(options or {}), "storage": "wide", "leaf_storage": storage})
     return _run_wide(plan, bindings)

@@ -63,7 +63,7 @@ def spec(name, scale=1.0):
     if name == "C2":
         return "einsum", C.hex_poisson(E=max(1, int(2_000_000 * scale)))
     if name == "C3":
-        return "kernel", C.tccg_kernel(ext=72)
+        return "kernel", C.tccg_kernel(ext=72, a_ext=max(1, int(72 * scale)))
     if name == "C4-f64":
         return "einsum", C.tensor_train(n=max(1, int(4096 * scale)))
     if name == "C4-f32":
@@ -139,7 +139,11 @@ class ClockSampler:
 
 class Workload:
     def __init__(self, name, rank, world, torch, fe, seed):
-        kind, payload = spec(name)
+        # weak scaling: the global problem is `world` copies of the config along
+        # its shard axis; each rank plans the global einsum (same canonical
+        # form family, same tuned transform) and runs its 1/world shard, which
+        # is exactly the single-GPU config.
+        kind, payload = spec(name, scale=world) if world > 1 else spec(name)
         full = fe.Plan(einsum=payload) if kind == "einsum" else fe.Plan(kernel=payload)
         self.full = full
         self.name = name
@@ -151,7 +155,8 @@ class Workload:
         self.transform = info["transform"]
         self.source = info["source"]
         self.key = full.info["key"]
-        self.flops = info["algorithmic_flops"]
+        self.flops = info["algorithmic_flops"]  # this rank's shard
+        self.global_flops = full.info["algorithmic_flops"]
         self.bytes = info["bytes"]
         self.ref_flops = info["reference_flops"]
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -246,7 +251,7 @@ def gpu_arm(args):
     per = {}
     rates = []
     for w, t in zip(loads, mean_t):
-        agg_flops = w.flops * world  # weak scaling: every rank runs its shard of the same size
+        agg_flops = w.global_flops  # the global (world x config) problem, one shard per rank
         gflops = agg_flops / t / 1e9
         rates.append(gflops)
         per[w.name] = {"ms": t * 1e3, "gflops": gflops, "gbs": w.bytes * world / t / 1e9,

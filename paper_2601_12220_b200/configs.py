@@ -63,16 +63,20 @@ def tccg(name="abcd-aebf-dfce", ext=72, dtype="float64"):
     return {"i_out": list("abcd"), "i_in": [list(a), list(b)], "args": [[A, B]]}
 
 
-def tccg_kernel(name="abcd-aebf-dfce", ext=72):
+def tccg_kernel(name="abcd-aebf-dfce", ext=72, a_ext=None):
     """C3 with the TCCG protocol's functional operands alpha*A+beta
-    (PAPER.md:1708-1716), as a .fk kernel."""
+    (PAPER.md:1708-1716), as a .fk kernel. ``a_ext`` overrides the extent of
+    output index a (the multi-GPU shard axis)."""
     a, b = TCCG_SIBLINGS[name]
-    dims = "x".join([str(ext)] * 4)
-    return (f"domain: a<{ext} b<{ext} c<{ext} d<{ext} e<{ext} f<{ext}\n"
+    lens = {s: ext for s in "abcdef"}
+    lens["a"] = a_ext or ext
+    da = "x".join(str(lens[s]) for s in a)
+    db = "x".join(str(lens[s]) for s in b)
+    return (f"domain: a<{lens['a']} b<{ext} c<{ext} d<{ext} e<{ext} f<{ext}\n"
             "def opA(p,q,r,s) := alpha[]*A[p,q,r,s] + beta[]\n"
             "def opB(p,q,r,s) := alpha[]*B[p,q,r,s] + beta[]\n"
-            f"array: A float64 {dims}\n"
-            f"array: B float64 {dims}\n"
+            f"array: A float64 {da}\n"
+            f"array: B float64 {db}\n"
             "array: alpha float64 scalar\n"
             "array: beta float64 scalar\n"
             f"stmt C[a,b,c,d] = sum([e,f], opA({','.join(a)})*opB({','.join(b)}))\n")

@@ -681,6 +681,131 @@ bool bind_gett(Plan& p, std::string* why) {
   return true;
 }
 
+// Tensor-train family: G1[i,j] G2[k,l] X[n,j,l] -> Y[n,i,k], 64^4 cores.
+bool bind_tt(Plan& p, std::string* why) {
+  const auto m = match_roles(p.canon.canonical, {"ij", "kl", "njl"}, "nik");
+  if (!m) {
+    *why = "notation is not ij,kl,njl->nik";
+    return false;
+  }
+  if (p.complex_mode) {
+    *why = "complex data";
+    return false;
+  }
+  const auto lens = feinsum::index_lengths(p.canon.canonical);
+  TTBinding t;
+  t.nb = lens.at(m->idx.at('n'));
+  t.NI = static_cast<int>(lens.at(m->idx.at('i')));
+  t.NJ = static_cast<int>(lens.at(m->idx.at('j')));
+  t.NK = static_cast<int>(lens.at(m->idx.at('k')));
+  t.NL = static_cast<int>(lens.at(m->idx.at('l')));
+  if (!tt_supported(t.NI, t.NJ, t.NK, t.NL)) {
+    *why = "cores are not 64x64";
+    return false;
+  }
+  const int n = p.skel.n();
+  int storage = -1;
+  for (int q = 0; q < p.skel.b(); ++q) {
+    const int ur = p.canon.sigma_row[q];
+    TTBinding::Row r{};
+    int* dst[3] = {&r.g1, &r.g2, &r.x};
+    for (int role = 0; role < 3; ++role) {
+      const OperandStatic& op = p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[m->slot[role]]];
+      if (op.kind != OPK_PLAIN) {
+        *why = "functional operand";
+        return false;
+      }
+      const int st = p.leaves[op.leaf].storage;
+      if ((st != ST_F64 && st != ST_F32) || (storage >= 0 && st != storage)) {
+        *why = "storage must be uniformly f64 or f32";
+        return false;
+      }
+      storage = st;
+      *dst[role] = op.leaf;
+    }
+    if (p.outputs[ur].storage != storage) {
+      *why = "output storage differs from the inputs";
+      return false;
+    }
+    r.out_row = ur;
+    t.rows.push_back(r);
+  }
+  t.fp32 = storage == ST_F32;
+  p.tt = std::move(t);
+  return true;
+}
+
+// Hex sum-factorised family (C2):
+//   B1[x,a,i] B2[x,b,m] B3[x,c,n] G[x,y,e,a,b,c] F1[y,a,j] F2[y,b,k] F3[y,c,l] u[e,j,k,l] -> y[e,i,m,n]
+// with the 1-D operators and G shared by every row (field).
+bool bind_hex(Plan& p, std::string* why) {
+  const BatchedEinsum& c = p.canon.canonical;
+  if (c.n() != 8 || p.complex_mode) {
+    *why = "not an 8-slot real einsum";
+    return false;
+  }
+  const auto m = match_roles(c, {"xai", "xbm", "xcn", "xyeabc", "yaj", "ybk", "ycl", "ejkl"}, "eimn");
+  if (!m) {
+    *why = "notation is not the sum-factorised hex operator";
+    return false;
+  }
+  const auto lens = feinsum::index_lengths(c);
+  HexBinding h;
+  h.E = lens.at(m->idx.at('e'));
+  h.ND = static_cast<int>(lens.at(m->idx.at('x')));
+  h.P = static_cast<int>(lens.at(m->idx.at('a')));
+  for (char r : std::string("bcijklmn"))
+    if (lens.at(m->idx.at(r)) != h.P) {
+      *why = "quadrature and dof extents differ";
+      return false;
+    }
+  if (lens.at(m->idx.at('y')) != h.ND || !hex_supported(h.ND, h.P, h.E, c.b())) {
+    *why = "no compiled instance (needs 3 directions, P = 5, even E, <= 8 fields)";
+    return false;
+  }
+  const int n = c.n();
+  // pattern slot -> kernel matrix index: slots 0..2 backward (B1..B3), 4..6 forward (F1..F3)
+  const int mat_of_slot[8] = {3, 4, 5, -1, 0, 1, 2, -1};
+  for (int q = 0; q < c.b(); ++q) {
+    const int ur = p.canon.sigma_row[q];
+    auto leaf_at = [&](int role) -> int {
+      const OperandStatic& op = p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[m->slot[role]]];
+      if (op.kind != OPK_PLAIN || p.leaves[op.leaf].storage != ST_F64) return -1;
+      return op.leaf;
+    };
+    for (int role = 0; role < 8; ++role) {
+      const int leaf = leaf_at(role);
+      if (leaf < 0) {
+        *why = "functional or non-f64 operand";
+        return false;
+      }
+      if (role == 7) {
+        h.u.push_back(leaf);
+      } else if (role == 3) {
+        if (h.g >= 0 && h.g != leaf) {
+          *why = "G differs between rows";
+          return false;
+        }
+        h.g = leaf;
+      } else {
+        int& slot = h.mats[mat_of_slot[role]];
+        if (slot >= 0 && slot != leaf) {
+          *why = "1-D operators differ between rows";
+          return false;
+        }
+        slot = leaf;
+      }
+    }
+    if (p.outputs[ur].storage != ST_F64) {
+      *why = "non-f64 output";
+      return false;
+    }
+    h.out_row.push_back(ur);
+  }
+  p.hex = std::move(h);
+  return true;
+}
+
 // ------------------------------------------------------------ path FLOPs --
 
 }  // namespace
@@ -869,7 +994,7 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
   }
 
   // kernel choice: forced > fact > first matching family > generic
-  std::vector<Family> order = {Family::fem_grad, Family::gett};
+  std::vector<Family> order = {Family::fem_grad, Family::gett, Family::tt, Family::hex};
   auto family_of = [](const std::string& t) -> std::optional<Family> {
     for (Family f : {Family::generic, Family::fem_grad, Family::gett, Family::tt, Family::hex})
       if (t == family_transform(f)) return f;
@@ -882,6 +1007,8 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
       case Family::generic: return true;
       case Family::fem_grad: return bind_fem(p, &why);
       case Family::gett: return bind_gett(p, &why);
+      case Family::tt: return bind_tt(p, &why);
+      case Family::hex: return bind_hex(p, &why);
       default: return false;
     }
   };
@@ -1105,6 +1232,52 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
       return;
     }
   }
+  if (plan.family == Family::hex) {
+    const HexBinding& h = plan.hex;
+    bool ok = aligned16(d_in[h.g]);
+    for (int u : h.u) ok = ok && aligned16(d_in[u]);
+    if (ok) {
+      HexLaunch L{};
+      L.E = h.E;
+      L.ND = h.ND;
+      L.P = h.P;
+      L.rows = static_cast<int>(h.u.size());
+      for (int k = 0; k < 6; ++k) L.mats[k] = static_cast<const double*>(d_in[h.mats[k]]);
+      L.G = static_cast<const double*>(d_in[h.g]);
+      for (size_t q = 0; q < h.u.size(); ++q) {
+        L.U[q] = static_cast<const double*>(d_in[h.u[q]]);
+        L.Y[q] = static_cast<double*>(d_out[h.out_row[q]]);
+      }
+      cuda_check(launch_hex(L, stream), "hex kernel");
+      return;
+    }
+  }
+  if (plan.family == Family::tt) {
+    const TTBinding& b = plan.tt;
+    bool ok = true;
+    for (const auto& r : b.rows) ok = ok && aligned16(d_in[r.x]) && aligned16(d_out[r.out_row]);
+    if (ok) {
+      for (const auto& r : b.rows) {
+        TTLaunch L{};
+        L.Nb = b.nb;
+        L.NI = b.NI;
+        L.NJ = b.NJ;
+        L.NK = b.NK;
+        L.NL = b.NL;
+        L.fp32 = b.fp32 ? 1 : 0;
+        L.G1 = d_in[r.g1];
+        L.G2 = d_in[r.g2];
+        L.X = d_in[r.x];
+        L.Y = d_out[r.out_row];
+        L.x_sj = b.NL;
+        L.x_sn = static_cast<std::int64_t>(b.NJ) * b.NL;
+        L.y_sn = static_cast<std::int64_t>(b.NI) * b.NK;
+        L.stages = meta_int(plan.meta, "stages", 2);
+        cuda_check(launch_tt(L, stream), "tt kernel");
+      }
+      return;
+    }
+  }
   cuda_check(launch_generic(g, stream), "generic kernel");
 }
 
@@ -1200,16 +1373,104 @@ std::string describe(const Plan& p) {
   return fejson::dump(v);
 }
 
+namespace {
+
+// Canonical index each family shards along (element / batch / outer-M axis).
+std::string shard_index_of(const Plan& p) {
+  const BatchedEinsum& c = p.canon.canonical;
+  auto role = [&](const std::vector<std::string>& in, const std::string& out, char r) -> std::string {
+    const auto m = match_roles(c, in, out);
+    return m ? p.canon.sigma_idx.at(m->idx.at(r)) : std::string();
+  };
+  switch (p.family) {
+    case Family::fem_grad: return role({"xre", "xij", "ej"}, "rei", 'e');
+    case Family::tt: return role({"ij", "kl", "njl"}, "nik", 'n');
+    case Family::hex:
+      return role({"xai", "xbm", "xcn", "xyeabc", "yaj", "ybk", "ycl", "ejkl"}, "eimn", 'e');
+    case Family::gett: {
+      // mo: the outer M index (first M index of the A slot)
+      const std::string names = p.gett.role_names;
+      const auto at = names.find("mo=");
+      const std::string mo = names.substr(at + 3, names.find(' ', at) - at - 3);
+      return p.canon.sigma_idx.at(mo);
+    }
+    case Family::generic: break;
+  }
+  return p.skel.i_out.empty() ? std::string() : p.skel.i_out[0];
+}
+
+}  // namespace
+
 std::unique_ptr<Plan> make_shard(const Plan& full, int rank, int world, const PlanOptions& opt, std::int64_t* lo,
                                  std::int64_t* hi, std::string* axis) {
-  (void)full;
-  (void)rank;
-  (void)world;
-  (void)opt;
-  (void)lo;
-  (void)hi;
-  (void)axis;
-  throw error(errc::usage, "sharding not implemented yet");
+  if (world < 1 || rank < 0 || rank >= world) throw error(errc::usage, "shard: need 0 <= rank < world");
+  const std::string ix = shard_index_of(full);
+  if (ix.empty()) throw error(errc::usage, "this einsum has no output index to shard along");
+  const auto lens = feinsum::index_lengths(full.skel);
+  const std::int64_t n = lens.at(ix);
+  // fem_grad / hex move elements in pairs (16-byte bulk-copy runs)
+  const std::int64_t unit = (full.family == Family::fem_grad || full.family == Family::hex) ? 2 : 1;
+  const std::int64_t units = n / unit;
+  std::int64_t a = units * rank / world * unit, b = units * (rank + 1) / world * unit;
+  if (rank == world - 1) b = n;
+  if (b <= a) throw error(errc::usage, "shard: axis " + ix + " (" + std::to_string(n) + ") is too short for " +
+                                           std::to_string(world) + " ranks");
+  *lo = a;
+  *hi = b;
+  *axis = ix;
+
+  // the same einsum with the axis restricted to [a, b)
+  BatchedEinsum e = full.skel;
+  for (auto& row : e.args)
+    for (int k = 0; k < e.n(); ++k)
+      for (size_t d = 0; d < e.i_in[k].size(); ++d)
+        if (e.i_in[k][d] == ix) row[k].shape[d] = b - a;
+  if (!feinsum::validate(e).empty())
+    throw error(errc::usage, "shard: an array is read both along and across axis " + ix);
+
+  PlanOptions o = opt;
+  o.force_transform = full.transform;
+  std::unique_ptr<Plan> s;
+  if (!full.functional) {
+    s = make_plan(e, o);
+  } else {
+    // slice each leaf on the axes its reads bind to sharded operand axes
+    std::map<std::string, ArrayMeta> arrays;
+    for (const auto& L : full.leaves) arrays[L.meta.name] = L.meta;
+    std::map<std::string, std::vector<bool>> sliced;  // leaf -> axes
+    for (const auto& m : feinsum::universe(full.skel)) {
+      std::vector<bool> op_axis(static_cast<size_t>(m.dim()), false);
+      for (int k = 0; k < full.skel.n(); ++k)
+        for (const auto& row : full.skel.args)
+          if (row[k].name == m.name)
+            for (size_t d = 0; d < full.skel.i_in[k].size(); ++d) op_axis[d] = op_axis[d] || full.skel.i_in[k][d] == ix;
+      const OperandExpr& op = full.operand_exprs.at(m.name);
+      std::function<void(const Expr&)> walk = [&](const Expr& x) {
+        for (const Expr& c : x.children) walk(c);
+        if (x.kind != Expr::Kind::access) return;
+        auto& flags = sliced[x.name];
+        flags.resize(x.subs.size(), false);
+        for (size_t d = 0; d < x.subs.size(); ++d) {
+          const auto pit = std::find(op.params.begin(), op.params.end(), x.subs[d]);
+          const size_t pk = static_cast<size_t>(pit - op.params.begin());
+          if (pk < op_axis.size() && op_axis[pk]) flags[d] = true;
+        }
+      };
+      walk(op.body);
+    }
+    for (auto& [name, flags] : sliced) {
+      auto& meta = arrays.at(name);
+      for (size_t d = 0; d < flags.size(); ++d)
+        if (flags[d]) {
+          if (meta.shape[d] != n) throw error(errc::usage, "shard: array " + name + " is not aligned with " + ix);
+          meta.shape[d] = b - a;
+        }
+    }
+    s = make_functional_plan(e, full.operand_exprs, arrays, o);
+  }
+  s->meta = full.meta;
+  s->source = "shard of " + full.source + " plan " + full.key;
+  return s;
 }
 
 }  // namespace feb200

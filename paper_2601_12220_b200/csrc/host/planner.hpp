@@ -85,6 +85,26 @@ struct GettBinding {
   std::vector<Row> rows;
 };
 
+// Roles of the tensor-train family: Y[n,i,k] = sum G1[i,j] G2[k,l] X[n,j,l].
+struct TTBinding {
+  std::int64_t nb = 0;
+  int NI = 0, NJ = 0, NK = 0, NL = 0;
+  bool fp32 = false;
+  struct Row {
+    int g1, g2, x, out_row;
+  };
+  std::vector<Row> rows;
+};
+
+// Roles of the hex sum-factorised family (C2).
+struct HexBinding {
+  std::int64_t E = 0;
+  int ND = 0, P = 0;
+  int mats[6] = {-1, -1, -1, -1, -1, -1};  // leaf of F1 F2 F3 B1 B2 B3
+  int g = -1;
+  std::vector<int> u, out_row;  // per canonical row
+};
+
 struct Plan {
   // ---- what is computed ----
   BatchedEinsum skel;  // the caller's einsum (skeleton if functional)
@@ -108,6 +128,8 @@ struct Plan {
   Family family = Family::generic;
   FemBinding fem;
   GettBinding gett;
+  TTBinding tt;
+  HexBinding hex;
 
   // ---- costs ----
   double alg_flops = 0, operand_flops = 0, bytes = 0, ref_flops = 0;

@@ -11,8 +11,9 @@
 // Why this shape on sm_100a: tcgen05 has no f64 kind, so FP64 tensor work is
 // mma.sync m8n8k4 (DMMA, SASS DMMA.8x8x4). Tiles are staged by TMA
 // (cp.async.bulk.tensor, 4-D boxes gather the strided GETT operands without a
-// transpose pass) into a multi-stage mbarrier ring with the 128-byte swizzle,
-// which makes the A-fragment reads conflict-free; one producer warp issues the
+// transpose pass) into a multi-stage mbarrier ring. Each DMMA k-chunk spans
+// 2 kB x 2 kA values, so A (64-byte kA rows, 64B swizzle) and B (16-byte kB
+// rows) fragment reads both hit the 2-wavefront minimum; one producer warp issues the
 // TMA, nine consumer warps (3x3 grid of 24x24 warp tiles over a 72x72 CTA tile)
 // run the DMMAs. The persistent grid walks output tiles in groups that share A
 // slices so L2 serves the reuse.
@@ -47,8 +48,8 @@ struct GettDev {
   int stages, group;
 };
 
-// 128-byte swizzle: 16-byte chunk index (bits 4-6) ^= row (bits 7-9)
-__device__ __forceinline__ std::uint32_t swz(std::uint32_t off) { return off ^ (((off >> 7) & 7u) << 4); }
+// 64-byte swizzle (TMA CU_TENSOR_MAP_SWIZZLE_64B): 16-byte chunk bits [4:5] ^= bits [7:8]
+__device__ __forceinline__ std::uint32_t swz64(std::uint32_t off) { return off ^ (((off >> 7) & 3u) << 4); }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1,
                                             int c2, int c3) {
@@ -110,9 +111,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int ka0 = static_cast<int>(ks % p.ka_steps) * KA;
         ptx::mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
         unsigned char* st = tiles + static_cast<size_t>(s) * 2 * kTileBytes;
-        // A dims (kA, kB, mi, mo); B dims (kB, no, kA, ni)
-        tma_load_4d(st, &tmA, &full[s], ka0, kb0, 0, static_cast<int>(mo));
-        tma_load_4d(st + kTileBytes, &tmB, &full[s], kb0, static_cast<int>(no), ka0, 0);
+        // A dims (kA, mi, kB, mo) -> image [kB][mi][kA]; B dims (kB, ni, kA, no) -> image [kA][ni][kB]
+        tma_load_4d(st, &tmA, &full[s], ka0, 0, kb0, static_cast<int>(mo));
+        tma_load_4d(st + kTileBytes, &tmB, &full[s], kb0, 0, ka0, static_cast<int>(no));
       }
     }
     return;
@@ -143,21 +144,22 @@ __global__ void __launch_bounds__(kThreads, 2)
       const unsigned char* sb = sa + kTileBytes;
 #pragma unroll
       for (int kc = 0; kc < KT / 4; ++kc) {
-        const int e_l = kc >> 1;              // kB within the stage
-        const int f = (kc & 1) * 4 + qk;      // kA within the stage
+        // k chunk of 4 = {kB 0,1} x {kA 2kc, 2kc+1}; lane's k = (e_l, f)
+        const int e_l = qk >> 1;
+        const int f = 2 * kc + (qk & 1);
         double af[3], bf[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           const int m = wm * 24 + i * 8 + qrow;
-          // A image: [mi][kB][kA] -> m*128 + e_l*64 + f*8
-          af[i] = *reinterpret_cast<const double*>(sa + swz(static_cast<std::uint32_t>(m * 128 + e_l * 64 + f * 8)));
+          // A image [kB][mi][kA] (64-byte rows, 64B swizzle): conflict-free 8 rows x 16 B
+          af[i] = *reinterpret_cast<const double*>(sa + swz64(static_cast<std::uint32_t>(e_l * BM * 64 + m * 64 + f * 8)));
           if (affA) af[i] = fma(aA, af[i], bA);
         }
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           const int n = wn * 24 + j * 8 + qrow;
-          // B image: [ni][kA][kB] -> n*128 + f*16 + e_l*8
-          bf[j] = *reinterpret_cast<const double*>(sb + swz(static_cast<std::uint32_t>(n * 128 + f * 16 + e_l * 8)));
+          // B image [kA][ni][kB] (16-byte rows): 8 rows x 16 B contiguous per kA plane
+          bf[j] = *reinterpret_cast<const double*>(sb + f * BN * 16 + n * 16 + e_l * 8);
           if (affB) bf[j] = fma(aB, bf[j], bB);
         }
 #pragma unroll
@@ -203,7 +205,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool make_map(CUtensorMap* map, const double* base, const std::uint64_t dims[4], const std::uint64_t strides_el[4],
-              const std::uint32_t box[4]) {
+              const std::uint32_t box[4], CUtensorMapSwizzle swizzle) {
   auto enc = encode_fn();
   if (!enc) return false;
   cuuint64_t gdim[4], gstride[3];
@@ -214,7 +216,7 @@ bool make_map(CUtensorMap* map, const double* base, const std::uint64_t dims[4],
   }
   for (int d = 1; d < 4; ++d) gstride[d - 1] = strides_el[d] * 8;
   const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), gdim, gstride, bdim, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -229,20 +231,20 @@ int launch_gett(const GettLaunch& L, void* stream) {
   if (!gett_supported(L.ext_mi, L.ext_ni, L.ext_ka, L.ext_kb)) return cudaErrorInvalidValue;
   CUtensorMap tmA, tmB;
   {
-    const std::uint64_t dims[4] = {static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_kb),
-                                   static_cast<std::uint64_t>(L.ext_mi), static_cast<std::uint64_t>(L.ext_mo)};
-    const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.a_kb), static_cast<std::uint64_t>(L.a_mi),
+    const std::uint64_t dims[4] = {static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_mi),
+                                   static_cast<std::uint64_t>(L.ext_kb), static_cast<std::uint64_t>(L.ext_mo)};
+    const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.a_mi), static_cast<std::uint64_t>(L.a_kb),
                                   static_cast<std::uint64_t>(L.a_mo)};
-    const std::uint32_t box[4] = {KA, KB, BM, 1};
-    if (!make_map(&tmA, L.A, dims, str, box)) return cudaErrorInvalidValue;
+    const std::uint32_t box[4] = {KA, BM, KB, 1};
+    if (!make_map(&tmA, L.A, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
   }
   {
-    const std::uint64_t dims[4] = {static_cast<std::uint64_t>(L.ext_kb), static_cast<std::uint64_t>(L.ext_no),
-                                   static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_ni)};
-    const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.b_no), static_cast<std::uint64_t>(L.b_ka),
-                                  static_cast<std::uint64_t>(L.b_ni)};
-    const std::uint32_t box[4] = {KB, 1, KA, BN};
-    if (!make_map(&tmB, L.B, dims, str, box)) return cudaErrorInvalidValue;
+    const std::uint64_t dims[4] = {static_cast<std::uint64_t>(L.ext_kb), static_cast<std::uint64_t>(L.ext_ni),
+                                   static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_no)};
+    const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.b_ni), static_cast<std::uint64_t>(L.b_ka),
+                                  static_cast<std::uint64_t>(L.b_no)};
+    const std::uint32_t box[4] = {KB, BN, KA, 1};
+    if (!make_map(&tmB, L.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
   }
   GettDev d{};
   d.mo = L.ext_mo;

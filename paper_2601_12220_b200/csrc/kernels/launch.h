@@ -211,39 +211,39 @@ int launch_gett(const GettLaunch& p, void* stream);
 bool gett_supported(std::int64_t ext_mi, std::int64_t ext_ni, std::int64_t ext_ka, std::int64_t ext_kb);
 
 // ---- K4: tensor-train layer  Y[n,i,k] = sum_{j,l} G1[i,j] G2[k,l] X[n,j,l] ----
+// Layouts: G1 [i,j], G2 [k,l] row-major; X [n,j,l] with unit l stride; Y [n,i,k].
 struct TTLaunch {
-  std::int64_t Nb;  // batch
+  std::int64_t Nb;  // batch (samples)
   int NI, NJ, NK, NL;
-  int rows;
-  int fp32;  // 1: float storage/compute, 0: double (DMMA)
-  const void* G1[kFemMaxRows];
-  const void* G2[kFemMaxRows];
-  const void* X[kFemMaxRows];
-  void* Y[kFemMaxRows];
-  // strides of the roles inside their arrays (canonical layouts vary)
-  std::int64_t g1_si, g1_sj, g2_sk, g2_sl, x_sn, x_sj, x_sl, y_sn, y_si, y_sk;
-  int variant;
+  int fp32;  // 1: float storage (fp64 accumulation), 0: double
+  const void* G1;
+  const void* G2;
+  const void* X;
+  void* Y;
+  std::int64_t x_sj, x_sn, y_sn;
+  int stages;
 };
 
 int launch_tt(const TTLaunch& p, void* stream);
+bool tt_supported(int NI, int NJ, int NK, int NL);
 
 // ---- K5: hex sum-factorized operator ----
-// y_q[e,i,m,n] = sum A1[x,a,i] A2[x,b,m] A3[x,c,n] G[x,y,e,a,b,c]
-//                    A1[y,a,j] A2[y,b,k] A3[y,c,l] u_q[e,j,k,l]
+// y_q[e,i,m,n] = sum B1[x,a,i] B2[x,b,m] B3[x,c,n] G[x,y,e,a,b,c]
+//                    F1[y,a,j] F2[y,b,k] F3[y,c,l] u_q[e,j,k,l]
+// (C2 uses B_d = F_d = A_d). Layouts as written, row-major.
 struct HexLaunch {
   std::int64_t E;
-  int ND;   // 3 directions
-  int P;    // points/dofs per direction (5 for P4)
-  int rows;
-  const double* A[3];  // [ND, P, P] each (direction, quad point, dof)
-  const double* G;     // [ND, ND, E, P, P, P]
-  const double* U[kFemMaxRows];
-  double* Y[kFemMaxRows];
-  // element stride / strides of the roles (canonical layouts vary)
-  int variant;
+  int ND;    // 3 directions
+  int P;     // points = dofs per direction (5 for P4)
+  int rows;  // fields, <= 8
+  const double* mats[6];  // F1 F2 F3 B1 B2 B3, each [ND, P, P]
+  const double* G;        // [ND, ND, E, P, P, P]
+  const double* U[8];
+  double* Y[8];
 };
 
 int launch_hex(const HexLaunch& p, void* stream);
+bool hex_supported(int nd, int p, std::int64_t E, int rows);
 
 // ---- utilities ----
 int device_sm_count(int* out);

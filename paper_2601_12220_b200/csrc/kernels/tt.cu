@@ -1,0 +1,252 @@
+// K4 — tensor-train layer  Y[n,i,k] = sum_{j,l} G1[i,j] G2[k,l] X[n,j,l]
+// (C4: n = 4096 samples, 64x64 cores), i.e. two chained 64^3 GEMMs per sample:
+//   T = X_n G2^T   (T[j,k] = sum_l X[j,l] G2[k,l])
+//   Y_n = G1 T     (Y[i,k] = sum_j G1[i,j] T[j,k])
+//
+// B200 design: persistent CTAs, G1/G2 staged once per CTA in shared memory;
+// each sample's X_n arrives by TMA (2-D boxes, 128-byte swizzle) in a
+// double-buffered mbarrier ring while the previous sample computes; T never
+// leaves shared memory (written transposed so GEMM 2 reads conflict-free
+// fragments); Y_n is stored straight from the DMMA accumulators with 16-byte
+// stores. Arithmetic: DMMA m8n8k4 (fp64 tensor cores); fp32 storage is
+// converted on the fragment load and accumulated in fp64 (accuracy well inside
+// the fp32 bar; throughput is the fp64 tensor rate).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <mutex>
+
+#include "launch.h"
+#include "ptx.cuh"
+
+namespace feb200 {
+
+namespace {
+
+constexpr int R = 64;                  // core size
+constexpr int kConsumerWarps = 8;      // 8 warps x (16 rows x 32 cols)
+constexpr int kThreads = 32 * (kConsumerWarps + 1);
+
+__device__ __forceinline__ std::uint32_t swz(std::uint32_t off) { return off ^ (((off >> 7) & 7u) << 4); }
+
+// Shared matrix of 64 rows stored as column panels of 128-byte rows (the TMA
+// 128B-swizzle image): element (r, c) -> panel c / P, row r, column c % P.
+template <typename T>
+struct Panels {
+  static constexpr int P = 128 / sizeof(T);        // columns per panel
+  static constexpr int kPanelBytes = R * 128;      // 8 KB, 1024-aligned
+  static constexpr int kBytes = kPanelBytes * (R / P);
+  __device__ static std::uint32_t off(int r, int c) {
+    return (c / P) * kPanelBytes + swz(static_cast<std::uint32_t>(r * 128 + (c % P) * sizeof(T)));
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ double ld(const unsigned char* base, int r, int c) {
+  return static_cast<double>(*reinterpret_cast<const T*>(base + Panels<T>::off(r, c)));
+}
+
+struct TTDev {
+  std::int64_t nb;
+  const void* G1;
+  const void* G2;
+  void* Y;
+  std::int64_t y_sn;  // Y sample stride (elements); rows are i*64 + k
+  int stages;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    tt_kernel(const __grid_constant__ TTDev p, const __grid_constant__ CUtensorMap tmX) {
+  using PT = Panels<T>;
+  using PD = Panels<double>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+  unsigned char* g1 = base;                  // G1 as double panels [i][j]
+  unsigned char* g2 = g1 + PD::kBytes;       // G2 as double panels [k][l]
+  unsigned char* ts = g2 + PD::kBytes;       // T^T as double panels [k][j]
+  unsigned char* xr = ts + PD::kBytes;       // X ring, native panels [j][l]
+  const int S = p.stages;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(xr + static_cast<size_t>(S) * PT::kBytes);
+  std::uint64_t* empty = full + S;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], kConsumerWarps);
+    }
+    ptx::fence_barrier_init();
+  }
+  // cores to shared memory as fp64 panels (once per CTA)
+  for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
+    const int r = t / R, c = t % R;
+    *reinterpret_cast<double*>(g1 + PD::off(r, c)) = static_cast<double>(static_cast<const T*>(p.G1)[t]);
+    *reinterpret_cast<double*>(g2 + PD::off(r, c)) = static_cast<double>(static_cast<const T*>(p.G2)[t]);
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    if (lane != 0) return;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    int it = 0;
+    for (std::int64_t n = blockIdx.x; n < p.nb; n += gridDim.x, ++it) {
+      const int s = it % S;
+      const std::uint32_t round = static_cast<std::uint32_t>(it / S);
+      ptx::mbar_wait(&empty[s], (round & 1u) ^ 1u);
+      ptx::mbar_arrive_expect_tx(&full[s], PT::kBytes);
+      for (int panel = 0; panel < R / PT::P; ++panel) {
+        unsigned char* dst = xr + static_cast<size_t>(s) * PT::kBytes + panel * PT::kPanelBytes;
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+                ptx::smem_addr(dst)),
+            "l"(&tmX), "r"(ptx::smem_addr(&full[s])), "r"(panel * PT::P), "r"(0), "r"(static_cast<int>(n))
+            : "memory");
+      }
+    }
+    return;
+  }
+
+  // consumers: warp w owns rows [16*(w/2), +16) x cols [32*(w%2), +32) of the 64x64 result
+  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
+  const int qr = lane >> 2, qk = lane & 3;
+  int it = 0;
+  for (std::int64_t n = blockIdx.x; n < p.nb; n += gridDim.x, ++it) {
+    const int s = it % S;
+    const std::uint32_t round = static_cast<std::uint32_t>(it / S);
+    ptx::mbar_wait(&full[s], round & 1u);
+    const unsigned char* xs = xr + static_cast<size_t>(s) * PT::kBytes;
+
+    // GEMM 1: T[j,k] = sum_l X[j,l] G2[k,l]   (m = j, n = k, k-dim = l)
+    double acc[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < R; k0 += 4) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) af[a] = ld<T>(xs, wr + a * 8 + qr, k0 + qk);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = ld<double>(g2, wc + b * 8 + qr, k0 + qk);
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) ptx::dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    // X stage consumed
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    // T^T to shared memory: T[j][k] -> ts(row k, col j)
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int j = wr + a * 8 + qr, k = wc + b * 8 + 2 * qk + v;
+          *reinterpret_cast<double*>(ts + PD::off(k, j)) = acc[a][b][v];
+        }
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+
+    // GEMM 2: Y[i,k] = sum_j G1[i,j] T[j,k]   (m = i, n = k, k-dim = j)
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < R; k0 += 4) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) af[a] = ld<double>(g1, wr + a * 8 + qr, k0 + qk);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = ld<double>(ts, wc + b * 8 + qr, k0 + qk);
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) ptx::dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    // every warp finished reading T before the next sample overwrites it
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+
+    T* y = static_cast<T*>(p.Y) + n * p.y_sn;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = wr + a * 8 + qr, k = wc + b * 8 + 2 * qk;
+        if constexpr (sizeof(T) == 8) {
+          __stcs(reinterpret_cast<double2*>(y + i * R + k), make_double2(acc[a][b][0], acc[a][b][1]));
+        } else {
+          __stcs(reinterpret_cast<float2*>(y + i * R + k),
+                 make_float2(static_cast<float>(acc[a][b][0]), static_cast<float>(acc[a][b][1])));
+        }
+      }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+template <typename T>
+int launch_t(const TTLaunch& L, cudaStream_t stream) {
+  using PT = Panels<T>;
+  using PD = Panels<double>;
+  auto enc = encoder();
+  if (!enc) return cudaErrorInvalidValue;
+  CUtensorMap tm;
+  // X viewed as (l, j, n): unit stride l, then j, then the sample stride
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(L.Nb)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(L.x_sj * sizeof(T)), static_cast<cuuint64_t>(L.x_sn * sizeof(T))};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(PT::P), static_cast<cuuint32_t>(R), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(&tm, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                         const_cast<void*>(L.X), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  TTDev d{};
+  d.nb = L.Nb;
+  d.G1 = L.G1;
+  d.G2 = L.G2;
+  d.Y = L.Y;
+  d.y_sn = L.y_sn;
+  d.stages = L.stages > 0 ? L.stages : 2;
+  const size_t smem = 1024 + 3 * PD::kBytes + static_cast<size_t>(d.stages) * PT::kBytes + 16 * d.stages;
+  cudaError_t e = cudaFuncSetAttribute(tt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  device_sm_count(&sms);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tt_kernel<T>, kThreads, smem);
+  std::int64_t grid = static_cast<std::int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+  if (grid > L.Nb) grid = L.Nb;
+  tt_kernel<T><<<static_cast<int>(grid), kThreads, smem, stream>>>(d, tm);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool tt_supported(int NI, int NJ, int NK, int NL) { return NI == R && NJ == R && NK == R && NL == R; }
+
+int launch_tt(const TTLaunch& L, void* stream) {
+  if (!tt_supported(L.NI, L.NJ, L.NK, L.NL) || L.Nb <= 0) return L.Nb == 0 ? cudaSuccess : cudaErrorInvalidValue;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return L.fp32 ? launch_t<float>(L, s) : launch_t<double>(L, s);
+}
+
+}  // namespace feb200

@@ -256,3 +256,73 @@ def test_gett_full_c3_exact_vs_torch(fe, torch_cuda):
     want = torch.einsum("aebf,dfce->abcd", A, B)
     torch.cuda.synchronize()
     assert torch.equal(out, want)
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", FP64_TOL), ("float32", 1e-5)])
+def test_tensor_train_small(fe, ref, torch_cuda, dtype, tol):
+    from paper_2601_12220_b200 import configs as C
+    e = C.tensor_train(n=6, dtype=dtype)
+    plan = fe.Plan(einsum=e)
+    assert plan.info["transform"] == "tt/v1"
+    b = ref.random_bindings(e, 12)
+    got = run_plan(torch_cuda, plan, b)
+    want = ref.evaluate(e, b)
+    assert rel_err(got[0], want[0]) <= tol
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", FP64_TOL), ("float32", 1e-5)])
+def test_tensor_train_full_vs_torch(fe, torch_cuda, dtype, tol):
+    """C4 at full size (n = 4096) against an fp64 torch.einsum of the same data."""
+    from paper_2601_12220_b200 import configs as C
+    torch = torch_cuda
+    plan = fe.Plan(einsum=C.tensor_train(n=4096, dtype=dtype))
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    G1 = torch.empty(64, 64, dtype=tdt, device="cuda")
+    G2 = torch.empty(64, 64, dtype=tdt, device="cuda")
+    X = torch.empty(4096, 64, 64, dtype=tdt, device="cuda")
+    for k, t in enumerate((G1, G2, X)):
+        fe.fill_dyadic(t, 30 + k)
+    (Y,) = plan(G1, G2, X)
+    want = torch.einsum("ij,kl,njl->nik", G1.double(), G2.double(), X.double())
+    err = ((Y.double() - want).abs() / want.abs().clamp(min=1.0)).max().item()
+    assert err <= tol
+
+
+def test_hex_sumfact_small(fe, ref, torch_cuda):
+    """C2's sum-factorised operator at oracle-sized extents."""
+    from paper_2601_12220_b200 import configs as C
+    for E, b in [(2, 1), (4, 3)]:
+        e = C.hex_poisson(E=E, b=b)
+        plan = fe.Plan(einsum=e)
+        assert plan.info["transform"] == "hex_sumfact/v1"
+        bind = ref.random_bindings(e, E + b)
+        got = run_plan(torch_cuda, plan, bind)
+        want = ref.evaluate(e, bind)
+        for g, w in zip(got, want):
+            assert rel_err(g, w) <= FP64_TOL, (E, b)
+
+
+def test_hex_sumfact_large_sampled(fe, torch_cuda):
+    """E = 200k elements, 8 fields (the C2 grid shape), checked on sampled
+    elements against an independent fp64 torch evaluation of the same einsum."""
+    from paper_2601_12220_b200 import configs as C
+    torch = torch_cuda
+    E = 200_000
+    plan = fe.Plan(einsum=C.hex_poisson(E=E, b=8))
+    assert plan.info["transform"] == "hex_sumfact/v1"
+    ins = []
+    for k, m in enumerate(plan.inputs):
+        t = torch.empty(m["shape"], dtype=torch.float64, device="cuda")
+        fe.fill_dyadic(t, 50 + k)
+        ins.append(t)
+    outs = plan(*ins)
+    names = [m["name"] for m in plan.inputs]
+    A1, A2, A3, G = (ins[names.index(n)] for n in ("A1", "A2", "A3", "G"))
+    idx = torch.randint(0, E, (64,), device="cuda")
+    Gs = G[:, :, idx]
+    for q in range(8):
+        u = ins[names.index(f"u{q + 1}")][idx]
+        want = torch.einsum("xai,xbm,xcn,xyeabc,yaj,ybk,ycl,ejkl->eimn", A1, A2, A3, Gs, A1, A2, A3, u)
+        got = outs[q][idx]
+        err = ((got - want).abs() / want.abs().clamp(min=1.0)).max().item()
+        assert err <= FP64_TOL, q

@@ -1148,7 +1148,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
     L.NR = f.NR;
     L.NI = f.NI;
     L.NJ = f.NJ;
-    L.stages = 4;
+    L.stages = meta_int(plan.meta, "stages", 4);
     std::vector<int> jl, dl;
     bool ok = true;
     int u = 0;
@@ -1184,10 +1184,8 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
     }
     for (size_t a = 0; a < dl.size(); ++a) L.D[a] = static_cast<const double*>(d_in[dl[a]]);
     L.coef = plan.d_coef;
-    const int te = f.NI == 10 ? 32 : (f.NI == 4 ? 64 : 16);
-    const std::int64_t ntiles = (f.E + te - 1) / te;
-    L.tile_e = te;
-    L.grid = static_cast<int>(std::min<std::int64_t>(ntiles, static_cast<std::int64_t>(plan.sm_count) * 2));
+    L.tile_e = f.NI == 10 ? 32 : (f.NI == 4 ? 64 : 16);
+    L.grid = meta_int(plan.meta, "grid", 0);  // 0: all resident CTAs
     if (ok) {
       cuda_check(launch_fem_grad(L, stream), "fem_grad kernel");
       return;
@@ -1224,8 +1222,8 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         L.b_alpha = r.b_alpha;
         L.b_beta = r.b_beta;
         L.coef = plan.d_coef;
-        L.stages = meta_int(plan.meta, "stages", 5);
-        L.group = meta_int(plan.meta, "group", 4);
+        L.stages = meta_int(plan.meta, "stages", 3);
+        L.group = meta_int(plan.meta, "group", 12);
         L.grid = meta_int(plan.meta, "grid", 0);
         cuda_check(launch_gett(L, stream), "gett kernel");
       }

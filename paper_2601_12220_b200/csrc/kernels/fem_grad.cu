@@ -2,7 +2,7 @@
 // (the C1/C5 configs), HBM-bound, fp64.
 //
 // B200 design (persistent, warp-specialised, TMA-fed):
-//   * grid = a multiple of the SM count; each CTA walks element tiles of TE
+//   * grid = resident CTAs on all SMs; each CTA walks element tiles of TE
 //     elements with a stride of gridDim.x;
 //   * warp 0 (one elected lane) is the producer: for every tile it arms the
 //     stage's mbarrier with the byte count and issues 1-D bulk copies
@@ -10,14 +10,13 @@
 //     contiguous runs of TE doubles per distinct J) and of every U leaf tile
 //     (TE*NJ contiguous doubles) into an S-stage shared-memory ring — inputs are
 //     read from HBM exactly once and shared J is staged once for all rows;
-//   * TE*NI consumer threads, thread (el, i): D_q[x,i,:] lives in registers
-//     (loaded once from a shared copy of D), U is read as double2 broadcasts,
-//     J as broadcasts; t[x] = D.u then y[r] = J^T t. Consecutive threads own
-//     consecutive (e, i), so every y_q[r, :, :] store is a fully coalesced
-//     256-byte warp transaction — no output staging needed;
-//   * functional U operands (e.g. s = u + 0.5 k, the C5 wave step) are fused:
-//     the producer stages each leaf tile and consumers combine them in
-//     registers, so s never exists in HBM (the K2 prologue).
+//   * functional U operands (s = u + 0.5 k, the C5 wave step) are combined
+//     ONCE per tile by the consumers into a double-buffered shared tile (the
+//     K2 prologue: s never exists in HBM, and no value is computed twice);
+//   * TE*NI consumer threads, thread (el, i): D_q[x,i,:] lives in registers,
+//     U is read as double2 broadcasts, J as broadcasts; t[x] = D.u then
+//     y[r] = J^T t. Consecutive threads own consecutive (e, i), so every
+//     y_q[r, :, :] store is a fully coalesced 256-byte warp transaction.
 // The operation order differs from the reference's (factorised contraction
 // path with FMA); parity is within 1e-12 relative.
 #include <cuda_runtime.h>
@@ -29,6 +28,11 @@ namespace feb200 {
 
 namespace {
 
+struct Coef {
+  double pre, post;  // 1.0 when absent (x * 1.0 == x exactly)
+  int sign;
+};
+
 template <int NX, int NR, int NI, int NJ, int TE, bool kPlainU>
 __global__ void __launch_bounds__(32 + TE * NI, 1)
     fem_grad_kernel(const __grid_constant__ FemGradLaunch p) {
@@ -36,15 +40,17 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
   static_assert(kConsumers % 32 == 0, "consumer threads must fill warps");
   constexpr int kConsumerWarps = kConsumers / 32;
   static_assert(NJ % 2 == 0, "U rows are read as double2");
+  constexpr int kUTile = TE * NJ;          // doubles per U tile
+  constexpr int kJTile = NX * NR * TE;     // doubles per J tile
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int S = p.stages;
-  const int j_tile = NX * NR * TE;        // doubles per distinct J per stage
-  const int u_tile = TE * NJ;             // doubles per U leaf per stage
-  const int stage_doubles = p.n_j * j_tile + p.n_u * u_tile;
-  double* dsm = reinterpret_cast<double*>(smem_raw);                 // D copies
-  double* ring = dsm + p.n_d * NX * NI * NJ;                          // stages
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(ring + static_cast<size_t>(S) * stage_doubles);
+  const int stage_doubles = p.n_j * kJTile + p.n_u * kUTile;
+  double* dsm = reinterpret_cast<double*>(smem_raw);                   // D copies
+  double* ring = dsm + p.n_d * NX * NI * NJ;                            // stages
+  double* ucomb = ring + static_cast<size_t>(S) * stage_doubles;        // [2][rows][TE*NJ]
+  Coef* coefs = reinterpret_cast<Coef*>(ucomb + (kPlainU ? 0 : 2 * p.rows * kUTile));
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(coefs + kFemMaxUTiles);
   std::uint64_t* empty = full + S;
 
   const int tid = threadIdx.x;
@@ -59,10 +65,16 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
     }
     ptx::fence_barrier_init();
   }
-  // D arrays to shared memory (tiny, L2-resident across CTAs)
   for (int t = tid; t < p.n_d * NX * NI * NJ; t += blockDim.x) {
     const int which = t / (NX * NI * NJ);
     dsm[t] = __ldg(p.D[which] + (t - which * NX * NI * NJ));
+  }
+  if (!kPlainU && tid < p.n_u) {
+    Coef c;
+    c.pre = p.u_pre[tid] >= 0 ? __ldg(p.coef + 2 * p.u_pre[tid]) : 1.0;
+    c.post = p.u_post[tid] >= 0 ? __ldg(p.coef + 2 * p.u_post[tid]) : 1.0;
+    c.sign = p.u_sign[tid];
+    coefs[tid] = c;
   }
   __syncthreads();
 
@@ -84,10 +96,10 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
       double* st = ring + static_cast<size_t>(s) * stage_doubles;
       for (int a = 0; a < p.n_j; ++a)
         for (int xr = 0; xr < NX * NR; ++xr)
-          ptx::bulk_g2s_hint(st + a * j_tile + xr * TE, p.J[a] + xr * E + e0, jb, &full[s], pol);
-      double* su = st + p.n_j * j_tile;
+          ptx::bulk_g2s_hint(st + a * kJTile + xr * TE, p.J[a] + xr * E + e0, jb, &full[s], pol);
+      double* su = st + p.n_j * kJTile;
       for (int u = 0; u < p.n_u; ++u)
-        ptx::bulk_g2s_hint(su + u * u_tile, p.U[u] + e0 * NJ, ub, &full[s], pol);
+        ptx::bulk_g2s_hint(su + u * kUTile, p.U[u] + e0 * NJ, ub, &full[s], pol);
     }
     return;
   }
@@ -104,10 +116,35 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
     const std::uint32_t round = static_cast<std::uint32_t>(it / S);
     ptx::mbar_wait(&full[s], round & 1u);
     const std::int64_t e0 = tile * TE;
-    const bool live = e0 + el < E;
     const double* st = ring + static_cast<size_t>(s) * stage_doubles;
-    const double* su = st + p.n_j * j_tile;
-    if (live) {
+    const double* su = st + p.n_j * kJTile;
+
+    // K2 prologue: combine every row's U leaves once per tile
+    const double* ubase;
+    int urow_stride;
+    if (kPlainU) {
+      ubase = su;
+      urow_stride = kUTile;  // row q reads leaf tile row_u_first[q] == q
+    } else {
+      double* uc = ucomb + (it & 1) * p.rows * kUTile;
+      for (int q = 0; q < p.rows; ++q) {
+        const int u0 = p.row_u_first[q], nt = p.row_u_count[q];
+        for (int v = c; v < kUTile; v += kConsumers) {
+          double acc = 0.0;
+          for (int k = 0; k < nt; ++k) {
+            const Coef cf = coefs[u0 + k];
+            const double x = __dmul_rn(__dmul_rn(cf.pre, su[(u0 + k) * kUTile + v]), cf.post);
+            acc = k == 0 ? x : (cf.sign > 0 ? __dadd_rn(acc, x) : __dsub_rn(acc, x));
+          }
+          uc[q * kUTile + v] = acc;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+      ubase = uc;
+      urow_stride = kUTile;
+    }
+
+    if (e0 + el < E) {
       for (int q = 0; q < p.rows; ++q) {
         if (p.row_d[q] != cur_d) {
           cur_d = p.row_d[q];
@@ -117,48 +154,20 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
 #pragma unroll
             for (int j = 0; j < NJ; ++j) dreg[x][j] = dq[(x * NI + i) * NJ + j];
         }
+        const double* ur = ubase + (kPlainU ? p.row_u_first[q] : q) * urow_stride + el * NJ;
         double t[NX];
 #pragma unroll
         for (int x = 0; x < NX; ++x) t[x] = 0.0;
-        const int u0 = p.row_u_first[q];
 #pragma unroll
         for (int j = 0; j < NJ; j += 2) {
-          double2 u;
-          if (kPlainU) {
-            u = *reinterpret_cast<const double2*>(su + u0 * u_tile + el * NJ + j);
-          } else {
-            u = make_double2(0.0, 0.0);
-            for (int k = 0; k < p.row_u_count[q]; ++k) {
-              const int ut = u0 + k;
-              double2 v = *reinterpret_cast<const double2*>(su + ut * u_tile + el * NJ + j);
-              if (p.u_pre[ut] >= 0) {
-                const double c0 = __ldg(p.coef + 2 * p.u_pre[ut]);
-                v.x = __dmul_rn(c0, v.x);
-                v.y = __dmul_rn(c0, v.y);
-              }
-              if (p.u_post[ut] >= 0) {
-                const double c1 = __ldg(p.coef + 2 * p.u_post[ut]);
-                v.x = __dmul_rn(v.x, c1);
-                v.y = __dmul_rn(v.y, c1);
-              }
-              if (k == 0) {
-                u = v;
-              } else if (p.u_sign[ut] > 0) {
-                u.x = __dadd_rn(u.x, v.x);
-                u.y = __dadd_rn(u.y, v.y);
-              } else {
-                u.x = __dsub_rn(u.x, v.x);
-                u.y = __dsub_rn(u.y, v.y);
-              }
-            }
-          }
+          const double2 u = *reinterpret_cast<const double2*>(ur + j);
 #pragma unroll
           for (int x = 0; x < NX; ++x) {
             t[x] = fma(dreg[x][j], u.x, t[x]);
             t[x] = fma(dreg[x][j + 1], u.y, t[x]);
           }
         }
-        const double* jt = st + p.row_j[q] * j_tile;
+        const double* jt = st + p.row_j[q] * kJTile;
         double* yq = p.Y[q];
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
@@ -176,16 +185,25 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
 
 template <int NX, int NR, int NI, int NJ, int TE>
 int launch_shape(const FemGradLaunch& p, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (static_cast<size_t>(p.n_d) * NX * NI * NJ +
-                                        static_cast<size_t>(p.stages) * (p.n_j * NX * NR * TE + p.n_u * TE * NJ)) +
-                      sizeof(std::uint64_t) * 2 * p.stages;
+  const bool plain = p.plain_u;
+  const size_t doubles = static_cast<size_t>(p.n_d) * NX * NI * NJ +
+                         static_cast<size_t>(p.stages) * (p.n_j * NX * NR * TE + p.n_u * TE * NJ) +
+                         (plain ? 0 : 2 * static_cast<size_t>(p.rows) * TE * NJ);
+  const size_t smem = sizeof(double) * doubles + sizeof(Coef) * kFemMaxUTiles + sizeof(std::uint64_t) * 2 * p.stages;
   auto run = [&](auto kern) -> int {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    kern<<<p.grid, 32 + TE * NI, smem, s>>>(p);
+    int sms = 148, per_sm = 1;
+    device_sm_count(&sms);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 + TE * NI, smem);
+    const std::int64_t ntiles = (p.E + TE - 1) / TE;
+    std::int64_t grid = static_cast<std::int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+    if (p.grid > 0) grid = p.grid;
+    if (grid > ntiles) grid = ntiles;
+    kern<<<static_cast<int>(grid), 32 + TE * NI, smem, s>>>(p);
     return cudaGetLastError();
   };
-  if (p.plain_u) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true>);
+  if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true>);
   return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false>);
 }
 

@@ -11,9 +11,10 @@
 // Why this shape on sm_100a: tcgen05 has no f64 kind, so FP64 tensor work is
 // mma.sync m8n8k4 (DMMA, SASS DMMA.8x8x4). Tiles are staged by TMA
 // (cp.async.bulk.tensor, 4-D boxes gather the strided GETT operands without a
-// transpose pass) into a multi-stage mbarrier ring. Each DMMA k-chunk spans
-// 2 kB x 2 kA values, so A (64-byte kA rows, 64B swizzle) and B (16-byte kB
-// rows) fragment reads both hit the 2-wavefront minimum; one producer warp issues the
+// transpose pass) into a 3-stage mbarrier ring, 64 k per stage as 8x8 boxes
+// with 64-byte inner rows (full-sector TMA requests). Each DMMA k-chunk spans
+// 2 kB x 2 kA values, so A and B fragment reads (both 64B-swizzled) hit the
+// 2-wavefront minimum; one producer warp issues the
 // TMA, nine consumer warps (3x3 grid of 24x24 warp tiles over a 72x72 CTA tile)
 // run the DMMAs. The persistent grid walks output tiles in groups that share A
 // slices so L2 serves the reuse.
@@ -32,11 +33,11 @@ namespace feb200 {
 namespace {
 
 constexpr int BM = 72, BN = 72;      // CTA tile (mi x ni)
-constexpr int KA = 8, KB = 2;        // k box: 8 of kA (128-byte rows with 2 of kB)
+constexpr int KA = 8, KB = 8;        // k box: 8 kA x 8 kB (64-byte rows on both operands)
 constexpr int KT = KA * KB;          // k per stage
 constexpr int kConsumerWarps = 9;
 constexpr int kThreads = 32 * (kConsumerWarps + 1);
-constexpr int kTileBytes = BM * KT * 8;  // 9216 = 9 x 1024 (swizzle atoms)
+constexpr int kTileBytes = BM * KT * 8;  // 36864 = 36 x 1024 (swizzle atoms)
 
 struct GettDev {
   std::int64_t mo, no;                  // tile counts (= extents of mo / no)
@@ -45,7 +46,7 @@ struct GettDev {
   double* C;
   const double* coef;
   int a_alpha, a_beta, b_alpha, b_beta;
-  int stages, group;
+  int stages, group;  // group: side of the square raster block (tiles sharing A/B slices in L2)
 };
 
 // 64-byte swizzle (TMA CU_TENSOR_MAP_SWIZZLE_64B): 16-byte chunk bits [4:5] ^= bits [7:8]
@@ -60,7 +61,7 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, s
       : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 1)
     gett_kernel(const __grid_constant__ GettDev p, const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -84,14 +85,18 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   __syncthreads();
 
-  // tile t -> (mo, no): groups of `group` mo-rows sweep all no (A reuse in L2)
+  // tile t -> (mo, no): square blocks of group x group tiles, so the ~150
+  // tiles in flight share `group` A slices and `group` B slices (fits L2)
   auto tile_coords = [&](std::int64_t t, std::int64_t& mo, std::int64_t& no) {
-    const std::int64_t per_group = static_cast<std::int64_t>(p.group) * p.no;
-    const std::int64_t g = t / per_group;
-    const std::int64_t r = t - g * per_group;
-    const std::int64_t rows = (g + 1) * p.group <= p.mo ? p.group : p.mo - g * p.group;
-    mo = g * p.group + r % rows;
-    no = r / rows;
+    const std::int64_t G = p.group;
+    const std::int64_t band = G * p.no;            // tiles in one band of G mo-rows
+    const std::int64_t bi = t / band, r = t - bi * band;
+    const std::int64_t rows = (bi + 1) * G <= p.mo ? G : p.mo - bi * G;
+    const std::int64_t bj = r / (rows * G), r2 = r - bj * rows * G;
+    const std::int64_t cols = (bj + 1) * G <= p.no ? G : p.no - bj * G;
+    mo = bi * G + r2 % rows;
+    no = bj * G + r2 / rows;
+    (void)cols;
   };
 
   if (warp == kConsumerWarps) {
@@ -111,7 +116,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int ka0 = static_cast<int>(ks % p.ka_steps) * KA;
         ptx::mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
         unsigned char* st = tiles + static_cast<size_t>(s) * 2 * kTileBytes;
-        // A dims (kA, mi, kB, mo) -> image [kB][mi][kA]; B dims (kB, ni, kA, no) -> image [kA][ni][kB]
+        // A dims (kA, mi, kB, mo) -> image [kB][mi][kA]; B dims (kB, ni, kA, no) -> image [kA][ni][kB];
+        // both with 64-byte rows under the 64B swizzle
         tma_load_4d(st, &tmA, &full[s], ka0, 0, kb0, static_cast<int>(mo));
         tma_load_4d(st + kTileBytes, &tmB, &full[s], kb0, 0, ka0, static_cast<int>(no));
       }
@@ -144,22 +150,22 @@ __global__ void __launch_bounds__(kThreads, 2)
       const unsigned char* sb = sa + kTileBytes;
 #pragma unroll
       for (int kc = 0; kc < KT / 4; ++kc) {
-        // k chunk of 4 = {kB 0,1} x {kA 2kc, 2kc+1}; lane's k = (e_l, f)
-        const int e_l = qk >> 1;
-        const int f = 2 * kc + (qk & 1);
+        // k chunk of 4 = {kB pair} x {kA pair}; lane's k = (e_l, f)
+        const int e_l = 2 * (kc >> 2) + (qk >> 1);
+        const int f = 2 * (kc & 3) + (qk & 1);
         double af[3], bf[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           const int m = wm * 24 + i * 8 + qrow;
-          // A image [kB][mi][kA] (64-byte rows, 64B swizzle): conflict-free 8 rows x 16 B
+          // A image [kB][mi][kA]: 8 rows x 16 B per kB plane -> 2 wavefronts (minimum)
           af[i] = *reinterpret_cast<const double*>(sa + swz64(static_cast<std::uint32_t>(e_l * BM * 64 + m * 64 + f * 8)));
           if (affA) af[i] = fma(aA, af[i], bA);
         }
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           const int n = wn * 24 + j * 8 + qrow;
-          // B image [kA][ni][kB] (16-byte rows): 8 rows x 16 B contiguous per kA plane
-          bf[j] = *reinterpret_cast<const double*>(sb + f * BN * 16 + n * 16 + e_l * 8);
+          // B image [kA][ni][kB]: same pattern with the roles of kA and kB swapped
+          bf[j] = *reinterpret_cast<const double*>(sb + swz64(static_cast<std::uint32_t>(f * BN * 64 + n * 64 + e_l * 8)));
           if (affB) bf[j] = fma(aB, bf[j], bB);
         }
 #pragma unroll
@@ -244,7 +250,7 @@ int launch_gett(const GettLaunch& L, void* stream) {
     const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.b_ni), static_cast<std::uint64_t>(L.b_ka),
                                   static_cast<std::uint64_t>(L.b_no)};
     const std::uint32_t box[4] = {KB, BN, KA, 1};
-    if (!make_map(&tmB, L.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    if (!make_map(&tmB, L.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
   }
   GettDev d{};
   d.mo = L.ext_mo;
@@ -261,8 +267,8 @@ int launch_gett(const GettLaunch& L, void* stream) {
   d.a_beta = L.a_beta;
   d.b_alpha = L.b_alpha;
   d.b_beta = L.b_beta;
-  d.stages = L.stages > 0 ? L.stages : 5;
-  d.group = L.group > 0 ? L.group : 4;
+  d.stages = L.stages > 0 ? L.stages : 3;
+  d.group = L.group > 0 ? L.group : 12;
   const size_t smem = 1024 + static_cast<size_t>(d.stages) * 2 * kTileBytes + 16 * d.stages;
   cudaError_t e = cudaFuncSetAttribute(gett_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

@@ -204,7 +204,7 @@ def test_vm_complex_sqrt(fe, ref, torch_cuda):
     assert rel_err(got[0], want[0]) <= FP64_TOL
 
 
-def _tccg_small(ref, fe, a_ext=2, c_ext=2, e_ext=4, f_ext=8):
+def _tccg_small(ref, fe, a_ext=2, c_ext=2, e_ext=8, f_ext=8):
     am = lambda n, s: {"name": n, "shape": s, "dtype": "float64"}  # noqa: E731
     lens = {"a": a_ext, "b": 72, "c": c_ext, "d": 72, "e": e_ext, "f": f_ext}
     return {"i_out": list("abcd"), "i_in": [list("aebf"), list("dfce")],
@@ -214,7 +214,7 @@ def _tccg_small(ref, fe, a_ext=2, c_ext=2, e_ext=4, f_ext=8):
 def test_gett_dmma_bit_exact_small(fe, ref, torch_cuda):
     """TCCG abcd-aebf-dfce through the TMA+DMMA kernel: dyadic inputs make
     every partial sum exact, so the result must equal the reference bitwise."""
-    for dims in [(2, 2, 4, 8), (3, 1, 2, 16), (1, 2, 6, 8)]:
+    for dims in [(2, 2, 8, 8), (3, 1, 8, 16), (1, 2, 16, 8)]:
         e = _tccg_small(ref, fe, *dims)
         plan = fe.Plan(einsum=e)
         assert plan.info["transform"] == "gett_dmma/v1", plan.info
@@ -226,10 +226,10 @@ def test_gett_dmma_bit_exact_small(fe, ref, torch_cuda):
 
 def test_gett_functional_operands(fe, ref, torch_cuda):
     """alpha*A+beta operands (TCCG protocol) fused into the DMMA fragment loads."""
-    fk = ("domain: a<2 b<72 c<2 d<72 e<4 f<8\n"
+    fk = ("domain: a<2 b<72 c<2 d<72 e<8 f<8\n"
           "def opA(p,q,r,s) := alpha[]*A[p,q,r,s] + beta[]\n"
           "def opB(p,q,r,s) := alpha[]*B[p,q,r,s] + beta[]\n"
-          "array: A float64 2x4x72x8\narray: B float64 72x8x2x4\n"
+          "array: A float64 2x8x72x8\narray: B float64 72x8x2x8\n"
           "array: alpha float64 scalar\narray: beta float64 scalar\n"
           "stmt C[a,b,c,d] = sum([e,f], opA(a,e,b,f)*opB(d,f,c,e))\n")
     info, arrays, b = _kernel_bindings(ref, fk, 4)

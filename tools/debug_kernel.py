@@ -10,7 +10,7 @@ from paper_2601_12220_b200 import feinsum as fe, configs as C
 which = sys.argv[1] if len(sys.argv) > 1 else "gett"
 am = lambda n, s, d="float64": {"name": n, "shape": s, "dtype": d}  # noqa: E731
 if which == "gett":
-    lens = {"a": 2, "b": 72, "c": 2, "d": 72, "e": 4, "f": 8}
+    lens = {"a": 2, "b": 72, "c": 2, "d": 72, "e": 8, "f": 8}
     e = {"i_out": list("abcd"), "i_in": [list("aebf"), list("dfce")],
          "args": [[am("A", [lens[s] for s in "aebf"]), am("B", [lens[s] for s in "dfce"])]]}
 elif which == "gett72":

@@ -111,6 +111,7 @@ PlanOptions parse_options(const std::string& json) {
   if (auto* x = v.find("transform")) o.force_transform = x->as_str();
   if (auto* x = v.find("canonicalize")) o.canonicalize = x->b;
   if (auto* x = v.find("dry_run")) o.dry_run = x->b;
+  if (auto* x = v.find("meta")) o.meta_override = x->as_str();
   return o;
 }
 
@@ -1041,6 +1042,7 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
         }
   }
   p.transform = family_transform(p.family);
+  if (!opt.meta_override.empty()) p.meta = opt.meta_override;
 
   // generic launch (always prepared: it is also the runtime fallback)
   std::vector<std::string> syms = e.i_out;
@@ -1062,6 +1064,14 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
   for (int r = 0; r < e.b(); ++r) g.out_storage[r] = p.outputs[r].storage;
 
   upload_tables(p, g, e, opt.dry_run);
+  if (!opt.dry_run && p.family == Family::gett) {
+    bool affine = false;
+    for (const auto& r : p.gett.rows) affine = affine || r.a_alpha >= 0 || r.b_alpha >= 0;
+    if (affine) {
+      const size_t n = static_cast<size_t>(p.gett.ext_mo * p.gett.ext_mi + p.gett.ext_no * p.gett.ext_ni);
+      cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_scratch), n * sizeof(double)), "cudaMalloc(gett scratch)");
+    }
+  }
 }
 
 int leaf_storage_for(const ArrayMeta& m, const PlanOptions& opt) {
@@ -1076,6 +1086,7 @@ int leaf_storage_for(const ArrayMeta& m, const PlanOptions& opt) {
 Plan::~Plan() {
   if (d_blob) cudaFree(d_blob);
   if (d_coef) cudaFree(d_coef);
+  if (d_scratch) cudaFree(d_scratch);
 }
 
 std::unique_ptr<Plan> make_plan(const BatchedEinsum& e, const PlanOptions& opt) {
@@ -1222,6 +1233,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         L.b_alpha = r.b_alpha;
         L.b_beta = r.b_beta;
         L.coef = plan.d_coef;
+        L.scratch = plan.d_scratch;
         L.stages = meta_int(plan.meta, "stages", 3);
         L.group = meta_int(plan.meta, "group", 12);
         L.grid = meta_int(plan.meta, "grid", 0);

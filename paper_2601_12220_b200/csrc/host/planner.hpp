@@ -46,6 +46,7 @@ struct PlanOptions {
   bool force_vm = false;      // internal: point evaluation (eval_expr)
   bool skip_range_check = false;
   bool dry_run = false;       // plan without touching the device (CPU tests)
+  std::string meta_override;  // tuner: run these parameters instead of the fact's
 };
 
 PlanOptions parse_options(const std::string& json);
@@ -138,6 +139,7 @@ struct Plan {
   int device = 0;
   void* d_blob = nullptr;
   double* d_coef = nullptr;
+  double* d_scratch = nullptr;  // family workspace (GETT affine K-sums)
   GenericLaunch gen{};  // pointers filled per execution
   int sm_count = 148;
 

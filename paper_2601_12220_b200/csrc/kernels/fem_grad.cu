@@ -155,18 +155,21 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
             for (int j = 0; j < NJ; ++j) dreg[x][j] = dq[(x * NI + i) * NJ + j];
         }
         const double* ur = ubase + (kPlainU ? p.row_u_first[q] : q) * urow_stride + el * NJ;
-        double t[NX];
+        // two accumulators per x (even / odd j): 2*NX independent FMA chains
+        double t[NX], t2[NX];
 #pragma unroll
-        for (int x = 0; x < NX; ++x) t[x] = 0.0;
+        for (int x = 0; x < NX; ++x) t[x] = t2[x] = 0.0;
 #pragma unroll
         for (int j = 0; j < NJ; j += 2) {
           const double2 u = *reinterpret_cast<const double2*>(ur + j);
 #pragma unroll
           for (int x = 0; x < NX; ++x) {
             t[x] = fma(dreg[x][j], u.x, t[x]);
-            t[x] = fma(dreg[x][j + 1], u.y, t[x]);
+            t2[x] = fma(dreg[x][j + 1], u.y, t2[x]);
           }
         }
+#pragma unroll
+        for (int x = 0; x < NX; ++x) t[x] += t2[x];
         const double* jt = st + p.row_j[q] * kJTile;
         double* yq = p.Y[q];
 #pragma unroll

@@ -46,6 +46,10 @@ struct GettDev {
   double* C;
   const double* coef;
   int a_alpha, a_beta, b_alpha, b_beta;
+  const double* rowA;  // sum_k A[m, k] per (mo, mi) (affine operands only)
+  const double* rowB;  // sum_k B[k, n] per (no, ni)
+  std::int64_t ext_mi, ext_ni;
+  double kdim;         // |K| = ext_ka * ext_kb
   int stages, group;  // group: side of the square raster block (tiles sharing A/B slices in L2)
 };
 
@@ -128,9 +132,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // -------------------------------- consumers --------------------------------
   const int wm = warp / 3, wn = warp % 3;  // 3x3 grid of 24x24 warp tiles
   const int qrow = lane >> 2, qk = lane & 3;
-  const bool affA = p.a_alpha >= 0, affB = p.b_alpha >= 0;
-  const double aA = affA ? p.coef[2 * p.a_alpha] : 1.0, bA = (affA && p.a_beta >= 0) ? p.coef[2 * p.a_beta] : 0.0;
-  const double aB = affB ? p.coef[2 * p.b_alpha] : 1.0, bB = (affB && p.b_beta >= 0) ? p.coef[2 * p.b_beta] : 0.0;
+  // functional operands (aA x + bA)(aB y + bB): the K-sum is hoisted out of
+  // the DMMA loop, C = aA aB S + aA bB rowA + bA aB rowB + bA bB |K|
+  const bool affine = p.a_alpha >= 0 || p.b_alpha >= 0;
+  const double aA = p.a_alpha >= 0 ? p.coef[2 * p.a_alpha] : 1.0;
+  const double bA = p.a_beta >= 0 ? p.coef[2 * p.a_beta] : 0.0;
+  const double aB = p.b_alpha >= 0 ? p.coef[2 * p.b_alpha] : 1.0;
+  const double bB = p.b_beta >= 0 ? p.coef[2 * p.b_beta] : 0.0;
 
   std::int64_t it = 0;
   for (std::int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -159,14 +167,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int m = wm * 24 + i * 8 + qrow;
           // A image [kB][mi][kA]: 8 rows x 16 B per kB plane -> 2 wavefronts (minimum)
           af[i] = *reinterpret_cast<const double*>(sa + swz64(static_cast<std::uint32_t>(e_l * BM * 64 + m * 64 + f * 8)));
-          if (affA) af[i] = fma(aA, af[i], bA);
         }
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           const int n = wn * 24 + j * 8 + qrow;
           // B image [kA][ni][kB]: same pattern with the roles of kA and kB swapped
           bf[j] = *reinterpret_cast<const double*>(sb + swz64(static_cast<std::uint32_t>(f * BN * 64 + n * 64 + e_l * 8)));
-          if (affB) bf[j] = fma(aB, bf[j], bB);
         }
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -186,6 +192,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < 3; ++j) {
         const int n = wn * 24 + j * 8 + 2 * qk;
         double* dst = cbase + m * p.c_mi + n * p.c_ni;
+        if (affine) {
+          const double ra = (bB != 0.0) ? p.rowA[mo * p.ext_mi + m] : 0.0;
+          const double k = bA * bB * p.kdim;
+          for (int v = 0; v < 2; ++v) {
+            const double rb = (bA != 0.0) ? p.rowB[no * p.ext_ni + n + v] : 0.0;
+            acc[i][j][v] = fma(aA * aB, acc[i][j][v], fma(aA * bB, ra, fma(bA * aB, rb, k)));
+          }
+        }
         if (p.c_ni == 1) {
           __stcs(reinterpret_cast<double2*>(dst), make_double2(acc[i][j][0], acc[i][j][1]));
         } else {
@@ -195,6 +209,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+}
+
+// rows[r0 * n1 + r1] = sum_{c0, c1} X[r0*s_r0 + r1*s_r1 + c0*s_c0 + c1*s_c1], one warp per row
+__global__ void rowsum_kernel(const double* __restrict__ X, double* __restrict__ rows, std::int64_t n0,
+                              std::int64_t n1, std::int64_t s_r0, std::int64_t s_r1, std::int64_t m0, std::int64_t m1,
+                              std::int64_t s_c0, std::int64_t s_c1) {
+  const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n0 * n1) return;
+  const std::int64_t r0 = warp / n1, r1 = warp % n1;
+  const double* base = X + r0 * s_r0 + r1 * s_r1;
+  double s = 0.0;
+  for (std::int64_t t = lane; t < m0 * m1; t += 32) s += __ldg(base + (t / m1) * s_c0 + (t % m1) * s_c1);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) rows[warp] = s;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -267,6 +296,20 @@ int launch_gett(const GettLaunch& L, void* stream) {
   d.a_beta = L.a_beta;
   d.b_alpha = L.b_alpha;
   d.b_beta = L.b_beta;
+  d.ext_mi = L.ext_mi;
+  d.ext_ni = L.ext_ni;
+  d.kdim = static_cast<double>(L.ext_ka) * static_cast<double>(L.ext_kb);
+  d.rowA = L.scratch;
+  d.rowB = L.scratch + L.ext_mo * L.ext_mi;
+  if (L.a_alpha >= 0 || L.b_alpha >= 0) {
+    if (!L.scratch) return cudaErrorInvalidValue;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const std::int64_t ra = L.ext_mo * L.ext_mi, rb = L.ext_no * L.ext_ni;
+    rowsum_kernel<<<static_cast<int>((ra * 32 + 255) / 256), 256, 0, st>>>(
+        L.A, L.scratch, L.ext_mo, L.ext_mi, L.a_mo, L.a_mi, L.ext_kb, L.ext_ka, L.a_kb, 1);
+    rowsum_kernel<<<static_cast<int>((rb * 32 + 255) / 256), 256, 0, st>>>(
+        L.B, L.scratch + ra, L.ext_no, L.ext_ni, L.b_no, L.b_ni, L.ext_ka, L.ext_kb, L.b_ka, 1);
+  }
   d.stages = L.stages > 0 ? L.stages : 3;
   d.group = L.group > 0 ? L.group : 12;
   const size_t smem = 1024 + static_cast<size_t>(d.stages) * 2 * kTileBytes + 16 * d.stages;

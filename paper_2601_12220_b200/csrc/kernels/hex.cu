@@ -15,11 +15,13 @@
 // into a double-buffered mbarrier ring, so G — the dominant traffic — is read
 // from HBM once and reused by all fields while the next pair is in flight.
 // The sweeps run on the FP64 pipe in four passes over 25-value planes held in
-// registers (two sweeps per pass where the plane contains both axes), with
-// the three directions and all fields of the pair in flight at once
-// (3 x 2 x 8 x 5 = 240 plane tasks per pass for 256 threads), so one pair
-// needs four CTA barriers. 5x5 operators are too small for DMMA tiles
-// (padding to 8x8 wastes 61%).
+// registers (two sweeps per pass where the plane contains both axes), with the
+// three directions and all fields of the pair in flight at once (240 plane
+// tasks for 256 threads), four CTA barriers per pair. Work cubes are padded to
+// rows of 6 doubles so every plane row moves as two 16-byte + one 8-byte
+// shared access, and lanes are assigned cube-fastest so that 8 consecutive
+// lanes' 16-byte accesses cover all 32 banks. 5x5 operators are too small for
+// DMMA tiles (padding to 8x8 wastes 61%).
 #include <cuda_runtime.h>
 
 #include "launch.h"
@@ -32,6 +34,10 @@ namespace {
 constexpr int P = 5;              // points / dofs per direction
 constexpr int P2 = P * P;         // 25
 constexpr int P3 = P * P * P;     // 125
+constexpr int RW = 6;             // padded row (16-byte multiple)
+constexpr int PL = P * RW;        // padded plane: 30 doubles
+constexpr int CB = P * PL;        // padded cube: 150 doubles (1200 B)
+constexpr int MS = 26;            // padded 5x5 operator stride (16-byte multiple)
 constexpr int ND = 3;             // directions
 constexpr int NE = 2;             // elements per pipeline stage (one bulk copy)
 constexpr int kMaxFields = 8;
@@ -46,15 +52,41 @@ struct HexDev {
   const double* mats[6];  // F1 F2 F3 (forward, [y][quad][dof]) B1 B2 B3 (backward, [x][quad][dof])
 };
 
+// 5x5 operator into registers (13 x 16-byte shared loads)
+__device__ __forceinline__ void load_op(const double* m, double (&c)[MS]) {
+#pragma unroll
+  for (int k = 0; k < MS; k += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(m + k);
+    c[k] = v.x;
+    c[k + 1] = v.y;
+  }
+}
+
+__device__ __forceinline__ void load_row(const double* p, double (&r)[P]) {
+  const double2 a = *reinterpret_cast<const double2*>(p);
+  const double2 b = *reinterpret_cast<const double2*>(p + 2);
+  r[0] = a.x;
+  r[1] = a.y;
+  r[2] = b.x;
+  r[3] = b.y;
+  r[4] = p[4];
+}
+
+__device__ __forceinline__ void store_row(double* p, const double (&r)[P]) {
+  *reinterpret_cast<double2*>(p) = make_double2(r[0], r[1]);
+  *reinterpret_cast<double2*>(p + 2) = make_double2(r[2], r[3]);
+  p[4] = r[4];
+}
+
 // forward operator entry M[o][i] = F[o][i]; backward M[o][i] = B[i][o]
 template <bool kBack>
-__device__ __forceinline__ double op(const double* m, int o, int i) {
-  return kBack ? m[i * P + o] : m[o * P + i];
+__device__ __forceinline__ double op(const double (&c)[MS], int o, int i) {
+  return kBack ? c[i * P + o] : c[o * P + i];
 }
 
 // v[r][.] <- M v[r][.] for every row r (contract the fast axis)
 template <bool kBack>
-__device__ __forceinline__ void rows5(double (&v)[P][P], const double* m) {
+__device__ __forceinline__ void rows5(double (&v)[P][P], const double (&c)[MS]) {
 #pragma unroll
   for (int r = 0; r < P; ++r) {
     double o[P];
@@ -62,7 +94,7 @@ __device__ __forceinline__ void rows5(double (&v)[P][P], const double* m) {
     for (int a = 0; a < P; ++a) {
       double s = 0.0;
 #pragma unroll
-      for (int b = 0; b < P; ++b) s = fma(op<kBack>(m, a, b), v[r][b], s);
+      for (int b = 0; b < P; ++b) s = fma(op<kBack>(c, a, b), v[r][b], s);
       o[a] = s;
     }
 #pragma unroll
@@ -72,19 +104,19 @@ __device__ __forceinline__ void rows5(double (&v)[P][P], const double* m) {
 
 // v[.][c] <- M v[.][c] for every column c (contract the slow axis)
 template <bool kBack>
-__device__ __forceinline__ void cols5(double (&v)[P][P], const double* m) {
+__device__ __forceinline__ void cols5(double (&v)[P][P], const double (&c)[MS]) {
 #pragma unroll
-  for (int c = 0; c < P; ++c) {
+  for (int col = 0; col < P; ++col) {
     double o[P];
 #pragma unroll
     for (int a = 0; a < P; ++a) {
       double s = 0.0;
 #pragma unroll
-      for (int b = 0; b < P; ++b) s = fma(op<kBack>(m, a, b), v[b][c], s);
+      for (int b = 0; b < P; ++b) s = fma(op<kBack>(c, a, b), v[b][col], s);
       o[a] = s;
     }
 #pragma unroll
-    for (int a = 0; a < P; ++a) v[a][c] = o[a];
+    for (int a = 0; a < P; ++a) v[a][col] = o[a];
   }
 }
 
@@ -92,28 +124,25 @@ __global__ void __launch_bounds__(kThreads, 1) hex_kernel(const __grid_constant_
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);
   const int R = p.rows;
-  const int nblk = NE * R;                            // (element, field) cubes per pair
-  // layout (doubles): mats | stage[2] = {G: 9*NE*P3, U: R*NE*P3} | WA[ND][nblk][P3] | WB[ND][nblk][P3]
-  double* mats = sm;                                  // 6 * ND * 25
-  double* stage0 = mats + 6 * ND * P2;
+  const int nblk = NE * R;  // (element, field) cubes per pair
+  // layout (doubles): ops[6][ND][MS] | stage[2] {G: 9*NE*P3, U: R*NE*P3} | WA[ND][nblk][CB] | WB[ND][nblk][CB]
+  double* ops = sm;
+  double* stage0 = ops + 6 * ND * MS;
   const int g_len = ND * ND * NE * P3, stage_len = g_len + R * NE * P3;
   double* WA = stage0 + 2 * stage_len;
-  double* WB = WA + ND * nblk * P3;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(WB + ND * nblk * P3);
+  double* WB = WA + ND * nblk * CB;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(WB + ND * nblk * CB);
 
-  for (int t = threadIdx.x; t < 6 * ND * P2; t += blockDim.x) mats[t] = __ldg(p.mats[t / (ND * P2)] + t % (ND * P2));
+  for (int t = threadIdx.x; t < 6 * ND * MS; t += blockDim.x) {
+    const int k = t / (ND * MS), d = (t / MS) % ND, e = t % MS;
+    ops[t] = e < P2 ? __ldg(p.mats[k] + d * P2 + e) : 0.0;
+  }
   if (threadIdx.x == 0) {
     ptx::mbar_init(&full[0], 1);
     ptx::mbar_init(&full[1], 1);
     ptx::fence_barrier_init();
   }
   __syncthreads();
-  const double* F1 = mats;
-  const double* F2 = mats + ND * P2;
-  const double* F3 = mats + 2 * ND * P2;
-  const double* B1 = mats + 3 * ND * P2;
-  const double* B2 = mats + 4 * ND * P2;
-  const double* B3 = mats + 5 * ND * P2;
 
   const std::int64_t npairs = p.E / NE;
   const std::uint32_t bytes = static_cast<std::uint32_t>(NE * P3 * 8);
@@ -127,14 +156,20 @@ __global__ void __launch_bounds__(kThreads, 1) hex_kernel(const __grid_constant_
   };
   if (threadIdx.x == 0 && blockIdx.x < npairs) issue(blockIdx.x, 0);
 
-  // plane task of this thread: direction d, cube blk = el*R + f, plane index pl
-  const int ntask = ND * nblk * P;
+  // plane task: direction d, plane index pl, cube blk = el*R + f (cube fastest)
+  const int ntask = ND * P * nblk;
   const int task = threadIdx.x;
   const bool active = task < ntask;
-  const int d = task / (nblk * P);
-  const int blk = (task / P) % nblk;
-  const int pl = task % P;
+  const int d = task / (P * nblk);
+  const int pl = (task / nblk) % P;
+  const int blk = task % nblk;
   const int el = blk / R, f = blk % R;
+  const double* opF1 = ops + (0 * ND + d) * MS;
+  const double* opF2 = ops + (1 * ND + d) * MS;
+  const double* opF3 = ops + (2 * ND + d) * MS;
+  const double* opB1 = ops + (3 * ND + d) * MS;
+  const double* opB2 = ops + (4 * ND + d) * MS;
+  const double* opB3 = ops + (5 * ND + d) * MS;
 
   int it = 0;
   for (std::int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x, ++it) {
@@ -144,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) hex_kernel(const __grid_constant_
     const double* G = stage0 + s * stage_len;  // [x*3+y][el][125]
     const double* U = G + g_len;               // [f][el][125]
     double v[P][P];
+    double c[MS];
 
     // pass 1 (direction y = d, plane j = pl): F3 along l, F2 along k
     if (active) {
@@ -152,75 +188,72 @@ __global__ void __launch_bounds__(kThreads, 1) hex_kernel(const __grid_constant_
       for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int l = 0; l < P; ++l) v[k][l] = in[k * P + l];
-      rows5<false>(v, F3 + d * P2);
-      cols5<false>(v, F2 + d * P2);
-      double* out = WA + (d * nblk + blk) * P3 + pl * P2;  // [j][b][c]
+      load_op(opF3, c);
+      rows5<false>(v, c);
+      load_op(opF2, c);
+      cols5<false>(v, c);
+      double* out = WA + (d * nblk + blk) * CB + pl * PL;  // [j][b][c]
 #pragma unroll
-      for (int b = 0; b < P; ++b)
-#pragma unroll
-        for (int c = 0; c < P; ++c) out[b * P + c] = v[b][c];
+      for (int b = 0; b < P; ++b) store_row(out + b * RW, v[b]);
     }
     __syncthreads();
     // pass 2 (direction y = d, plane b = pl): F1 along j -> t_y[a][b][c]
     if (active) {
-      const double* in = WA + (d * nblk + blk) * P3 + pl * P;
+      const double* in = WA + (d * nblk + blk) * CB + pl * RW;
 #pragma unroll
-      for (int j = 0; j < P; ++j)
+      for (int j = 0; j < P; ++j) load_row(in + j * PL, v[j]);
+      load_op(opF1, c);
+      cols5<false>(v, c);
+      double* out = WB + (d * nblk + blk) * CB + pl * RW;
 #pragma unroll
-        for (int c = 0; c < P; ++c) v[j][c] = in[j * P2 + c];
-      cols5<false>(v, F1 + d * P2);
-      double* out = WB + (d * nblk + blk) * P3 + pl * P;
-#pragma unroll
-      for (int a = 0; a < P; ++a)
-#pragma unroll
-        for (int c = 0; c < P; ++c) out[a * P2 + c] = v[a][c];
+      for (int a = 0; a < P; ++a) store_row(out + a * PL, v[a]);
     }
     __syncthreads();
     // pass 3 (direction x = d, plane b = pl): q_x = sum_y G[x,y] t_y, B1^T along a -> i
     if (active) {
+      const double* g = G + (d * ND * NE + el) * P3 + pl * P;
 #pragma unroll
-      for (int a = 0; a < P; ++a)
+      for (int a = 0; a < P; ++a) {
+        double t0[P], t1[P], t2[P];
+        load_row(WB + (0 * nblk + blk) * CB + a * PL + pl * RW, t0);
+        load_row(WB + (1 * nblk + blk) * CB + a * PL + pl * RW, t1);
+        load_row(WB + (2 * nblk + blk) * CB + a * PL + pl * RW, t2);
 #pragma unroll
-        for (int c = 0; c < P; ++c) {
-          const int pt = a * P2 + pl * P + c;
-          double q = 0.0;
-#pragma unroll
-          for (int y = 0; y < ND; ++y)
-            q = fma(G[((d * ND + y) * NE + el) * P3 + pt], WB[(y * nblk + blk) * P3 + pt], q);
-          v[a][c] = q;
+        for (int cc = 0; cc < P; ++cc) {
+          double q = g[a * P2 + cc] * t0[cc];
+          q = fma(g[NE * P3 + a * P2 + cc], t1[cc], q);
+          v[a][cc] = fma(g[2 * NE * P3 + a * P2 + cc], t2[cc], q);
         }
-      cols5<true>(v, B1 + d * P2);
-      double* out = WA + (d * nblk + blk) * P3 + pl * P;  // [i][b][c]
+      }
+      load_op(opB1, c);
+      cols5<true>(v, c);
+      double* out = WA + (d * nblk + blk) * CB + pl * RW;  // [i][b][c]
 #pragma unroll
-      for (int i = 0; i < P; ++i)
-#pragma unroll
-        for (int c = 0; c < P; ++c) out[i * P2 + c] = v[i][c];
+      for (int i = 0; i < P; ++i) store_row(out + i * PL, v[i]);
     }
     __syncthreads();
     // pass 4 (direction x = d, plane i = pl): B2^T along b -> m, B3^T along c -> n
     if (active) {
-      const double* in = WA + (d * nblk + blk) * P3 + pl * P2;
+      const double* in = WA + (d * nblk + blk) * CB + pl * PL;
 #pragma unroll
-      for (int b = 0; b < P; ++b)
+      for (int b = 0; b < P; ++b) load_row(in + b * RW, v[b]);
+      load_op(opB2, c);
+      cols5<true>(v, c);
+      load_op(opB3, c);
+      rows5<true>(v, c);
+      double* out = WB + (d * nblk + blk) * CB + pl * PL;  // partial y_x[i][m][n]
 #pragma unroll
-        for (int c = 0; c < P; ++c) v[b][c] = in[b * P + c];
-      cols5<true>(v, B2 + d * P2);
-      rows5<true>(v, B3 + d * P2);
-      double* out = WB + (d * nblk + blk) * P3 + pl * P2;  // partial y_x[i][m][n]
-#pragma unroll
-      for (int m = 0; m < P; ++m)
-#pragma unroll
-        for (int n = 0; n < P; ++n) out[m * P + n] = v[m][n];
+      for (int m = 0; m < P; ++m) store_row(out + m * RW, v[m]);
     }
     __syncthreads();
-    // sum the three direction partials and store (consecutive threads write
-    // consecutive doubles of one field's pair run)
+    // sum the three direction partials; consecutive threads write consecutive
+    // doubles of one field's 250-double pair run
     const std::int64_t e0 = pair * NE;
     for (int t = threadIdx.x; t < nblk * P3; t += blockDim.x) {
       const int ff = t / (NE * P3), rem = t % (NE * P3);
       const int ee = rem / P3, pt = rem % P3;
-      const int b2 = ee * R + ff;
-      const double y = WB[b2 * P3 + pt] + WB[(nblk + b2) * P3 + pt] + WB[(2 * nblk + b2) * P3 + pt];
+      const int off = (ee * R + ff) * CB + (pt / P2) * PL + ((pt / P) % P) * RW + pt % P;
+      const double y = WB[off] + WB[nblk * CB + off] + WB[2 * nblk * CB + off];
       __stcs(p.Y[ff] + e0 * P3 + rem, y);
     }
   }
@@ -245,7 +278,7 @@ int launch_hex(const HexLaunch& L, void* stream) {
   }
   for (int k = 0; k < 6; ++k) d.mats[k] = L.mats[k];
   const int R = L.rows;
-  const size_t doubles = 6 * ND * P2 + 2 * (ND * ND * NE * P3 + R * NE * P3) + 2 * ND * NE * R * P3;
+  const size_t doubles = 6 * ND * MS + 2 * (ND * ND * NE * P3 + R * NE * P3) + 2 * ND * NE * R * CB;
   const size_t smem = doubles * 8 + 16;
   cudaError_t e = cudaFuncSetAttribute(hex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

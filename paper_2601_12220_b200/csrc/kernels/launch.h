@@ -204,6 +204,7 @@ struct GettLaunch {
   // optional affine prologue: value = coef[alpha] * x + coef[beta] (-1 = none)
   int a_alpha, a_beta, b_alpha, b_beta;
   const double* coef;
+  double* scratch;  // ext_mo*ext_mi + ext_no*ext_ni doubles (affine operands' K-sums)
   int stages, group, grid;
 };
 

@@ -3,14 +3,17 @@
 //   T = X_n G2^T   (T[j,k] = sum_l X[j,l] G2[k,l])
 //   Y_n = G1 T     (Y[i,k] = sum_j G1[i,j] T[j,k])
 //
-// B200 design: persistent CTAs, G1/G2 staged once per CTA in shared memory;
-// each sample's X_n arrives by TMA (2-D boxes, 128-byte swizzle) in a
-// double-buffered mbarrier ring while the previous sample computes; T never
-// leaves shared memory (written transposed so GEMM 2 reads conflict-free
-// fragments); Y_n is stored straight from the DMMA accumulators with 16-byte
-// stores. Arithmetic: DMMA m8n8k4 (fp64 tensor cores); fp32 storage is
-// converted on the fragment load and accumulated in fp64 (accuracy well inside
-// the fp32 bar; throughput is the fp64 tensor rate).
+// B200 design: persistent CTAs, G1/G2 staged once per CTA in shared memory as
+// fp64 panels; samples are processed two at a time so each of the 8 DMMA warps
+// owns a 32x32 tile in both GEMMs (GEMM 1 on the stacked [X_a; X_b] (128x64),
+// GEMM 2 on [T_a | T_b] (64x128)) — 0.5 fragment loads per DMMA. X pairs arrive
+// by TMA (2-D boxes, 128-byte swizzle) in a double-buffered mbarrier ring while
+// the previous pair computes; T never leaves shared memory (fp64 samples write
+// T^T over their consumed X stage; fp32 samples use a separate T buffer) and is
+// stored transposed so GEMM 2's fragments are conflict-free; Y goes straight
+// from the accumulators with 16-byte stores. Arithmetic: DMMA m8n8k4 (fp64
+// tensor cores); fp32 storage is converted on the fragment load and
+// accumulated in fp64.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -26,13 +29,14 @@ namespace feb200 {
 namespace {
 
 constexpr int R = 64;                  // core size
-constexpr int kConsumerWarps = 8;      // 8 warps x (16 rows x 32 cols)
+constexpr int kConsumerWarps = 8;      // 8 warps x (32 x 32) per GEMM
 constexpr int kThreads = 32 * (kConsumerWarps + 1);
+constexpr int kPair = 2;               // samples per iteration
 
 __device__ __forceinline__ std::uint32_t swz(std::uint32_t off) { return off ^ (((off >> 7) & 7u) << 4); }
 
-// Shared matrix of 64 rows stored as column panels of 128-byte rows (the TMA
-// 128B-swizzle image): element (r, c) -> panel c / P, row r, column c % P.
+// 64-row matrix stored as column panels of 128-byte rows (the TMA 128B-swizzle
+// image): element (r, c) -> panel c / P, row r, column c % P.
 template <typename T>
 struct Panels {
   static constexpr int P = 128 / sizeof(T);        // columns per panel
@@ -54,7 +58,6 @@ struct TTDev {
   const void* G2;
   void* Y;
   std::int64_t y_sn;  // Y sample stride (elements); rows are i*64 + k
-  int stages;
 };
 
 template <typename T>
@@ -62,26 +65,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     tt_kernel(const __grid_constant__ TTDev p, const __grid_constant__ CUtensorMap tmX) {
   using PT = Panels<T>;
   using PD = Panels<double>;
+  constexpr bool kInPlaceT = sizeof(T) == 8;       // T^T overwrites the consumed X stage
+  constexpr int kStageBytes = kPair * PT::kBytes;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
-  unsigned char* g1 = base;                  // G1 as double panels [i][j]
-  unsigned char* g2 = g1 + PD::kBytes;       // G2 as double panels [k][l]
-  unsigned char* ts = g2 + PD::kBytes;       // T^T as double panels [k][j]
-  unsigned char* xr = ts + PD::kBytes;       // X ring, native panels [j][l]
-  const int S = p.stages;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(xr + static_cast<size_t>(S) * PT::kBytes);
-  std::uint64_t* empty = full + S;
+  unsigned char* g1 = base;                          // G1 [i][j] fp64 panels
+  unsigned char* g2 = g1 + PD::kBytes;               // G2 [k][l] fp64 panels
+  unsigned char* xr = g2 + PD::kBytes;               // 2 stages x 2 samples of X
+  unsigned char* tbuf = xr + 2 * kStageBytes;        // fp32 only: T^T for 2 samples
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(tbuf + (kInPlaceT ? 0 : kPair * PD::kBytes));
+  std::uint64_t* empty = full + 2;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
+    for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], kConsumerWarps);
     }
     ptx::fence_barrier_init();
   }
-  // cores to shared memory as fp64 panels (once per CTA)
   for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
     const int r = t / R, c = t % R;
     *reinterpret_cast<double*>(g1 + PD::off(r, c)) = static_cast<double>(static_cast<const T*>(p.G1)[t]);
@@ -89,103 +92,110 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
+  const std::int64_t npairs = (p.nb + kPair - 1) / kPair;
   if (warp == kConsumerWarps) {
     if (lane != 0) return;
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
     int it = 0;
-    for (std::int64_t n = blockIdx.x; n < p.nb; n += gridDim.x, ++it) {
-      const int s = it % S;
-      const std::uint32_t round = static_cast<std::uint32_t>(it / S);
-      ptx::mbar_wait(&empty[s], (round & 1u) ^ 1u);
-      ptx::mbar_arrive_expect_tx(&full[s], PT::kBytes);
-      for (int panel = 0; panel < R / PT::P; ++panel) {
-        unsigned char* dst = xr + static_cast<size_t>(s) * PT::kBytes + panel * PT::kPanelBytes;
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
-                ptx::smem_addr(dst)),
-            "l"(&tmX), "r"(ptx::smem_addr(&full[s])), "r"(panel * PT::P), "r"(0), "r"(static_cast<int>(n))
-            : "memory");
-      }
+    for (std::int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
+      const int s = it & 1;
+      ptx::mbar_wait(&empty[s], ((it >> 1) & 1u) ^ 1u);
+      ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
+      for (int smp = 0; smp < kPair; ++smp)
+        for (int panel = 0; panel < R / PT::P; ++panel) {
+          unsigned char* dst = xr + s * kStageBytes + smp * PT::kBytes + panel * PT::kPanelBytes;
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+                  ptx::smem_addr(dst)),
+              "l"(&tmX), "r"(ptx::smem_addr(&full[s])), "r"(panel * PT::P), "r"(0),
+              "r"(static_cast<int>(pr * kPair + smp))
+              : "memory");
+        }
     }
     return;
   }
 
-  // consumers: warp w owns rows [16*(w/2), +16) x cols [32*(w%2), +32) of the 64x64 result
-  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
   const int qr = lane >> 2, qk = lane & 3;
+  // GEMM 1 tile: stacked rows [32*(w/2), +32) (sample (w/2)/2), cols [32*(w%2), +32)
+  const int smp = warp >> 2;
+  const int r1 = (warp >> 1) * 32 - smp * R, c1 = (warp & 1) * 32;
+  // GEMM 2 tile (same sample): rows i [32*(w%2), +32), cols k [32*((w>>1)&1), +32)
+  const int r2 = (warp & 1) * 32, c2 = ((warp >> 1) & 1) * 32;
   int it = 0;
-  for (std::int64_t n = blockIdx.x; n < p.nb; n += gridDim.x, ++it) {
-    const int s = it % S;
-    const std::uint32_t round = static_cast<std::uint32_t>(it / S);
-    ptx::mbar_wait(&full[s], round & 1u);
-    const unsigned char* xs = xr + static_cast<size_t>(s) * PT::kBytes;
+  for (std::int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
+    const int s = it & 1;
+    ptx::mbar_wait(&full[s], (it >> 1) & 1u);
+    unsigned char* xs = xr + s * kStageBytes + smp * PT::kBytes;
+    unsigned char* ts = kInPlaceT ? xs : tbuf + smp * PD::kBytes;
 
-    // GEMM 1: T[j,k] = sum_l X[j,l] G2[k,l]   (m = j, n = k, k-dim = l)
-    double acc[2][4][2];
+    double acc[4][4][2];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll 4
+    // GEMM 1: T[j,k] = sum_l X[j,l] G2[k,l]
+#pragma unroll 2
     for (int k0 = 0; k0 < R; k0 += 4) {
-      double af[2], bf[4];
+      double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) af[a] = ld<T>(xs, wr + a * 8 + qr, k0 + qk);
+      for (int a = 0; a < 4; ++a) af[a] = ld<T>(xs, r1 + a * 8 + qr, k0 + qk);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = ld<double>(g2, wc + b * 8 + qr, k0 + qk);
+      for (int b = 0; b < 4; ++b) bf[b] = ld<double>(g2, c1 + b * 8 + qr, k0 + qk);
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) ptx::dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    // X stage consumed
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&empty[s]);
-    // T^T to shared memory: T[j][k] -> ts(row k, col j)
+    // all X of the pair consumed before T^T may overwrite it
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int j = wr + a * 8 + qr, k = wc + b * 8 + 2 * qk + v;
+          const int j = r1 + a * 8 + qr, k = c1 + b * 8 + 2 * qk + v;
           *reinterpret_cast<double*>(ts + PD::off(k, j)) = acc[a][b][v];
         }
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
 
-    // GEMM 2: Y[i,k] = sum_j G1[i,j] T[j,k]   (m = i, n = k, k-dim = j)
+    // GEMM 2: Y[i,k] = sum_j G1[i,j] T[j,k]
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll 4
+#pragma unroll 2
     for (int k0 = 0; k0 < R; k0 += 4) {
-      double af[2], bf[4];
+      double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) af[a] = ld<double>(g1, wr + a * 8 + qr, k0 + qk);
+      for (int a = 0; a < 4; ++a) af[a] = ld<double>(g1, r2 + a * 8 + qr, k0 + qk);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = ld<double>(ts, wc + b * 8 + qr, k0 + qk);
+      for (int b = 0; b < 4; ++b) bf[b] = ld<double>(ts, c2 + b * 8 + qr, k0 + qk);
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) ptx::dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    // every warp finished reading T before the next sample overwrites it
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    // the stage (X, and T^T when in place) is free once every warp has read it
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
 
-    T* y = static_cast<T*>(p.Y) + n * p.y_sn;
+    const std::int64_t n = pr * kPair + smp;
+    if (n < p.nb) {
+      T* y = static_cast<T*>(p.Y) + n * p.y_sn;
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int i = wr + a * 8 + qr, k = wc + b * 8 + 2 * qk;
-        if constexpr (sizeof(T) == 8) {
-          __stcs(reinterpret_cast<double2*>(y + i * R + k), make_double2(acc[a][b][0], acc[a][b][1]));
-        } else {
-          __stcs(reinterpret_cast<float2*>(y + i * R + k),
-                 make_float2(static_cast<float>(acc[a][b][0]), static_cast<float>(acc[a][b][1])));
+        for (int b = 0; b < 4; ++b) {
+          const int i = r2 + a * 8 + qr, k = c2 + b * 8 + 2 * qk;
+          if constexpr (sizeof(T) == 8) {
+            __stcs(reinterpret_cast<double2*>(y + i * R + k), make_double2(acc[a][b][0], acc[a][b][1]));
+          } else {
+            __stcs(reinterpret_cast<float2*>(y + i * R + k),
+                   make_float2(static_cast<float>(acc[a][b][0]), static_cast<float>(acc[a][b][1])));
+          }
         }
-      }
+    }
   }
 }
 
@@ -225,16 +235,17 @@ int launch_t(const TTLaunch& L, cudaStream_t stream) {
   d.G2 = L.G2;
   d.Y = L.Y;
   d.y_sn = L.y_sn;
-  d.stages = L.stages > 0 ? L.stages : 2;
-  const size_t smem = 1024 + 3 * PD::kBytes + static_cast<size_t>(d.stages) * PT::kBytes + 16 * d.stages;
+  constexpr bool kInPlaceT = sizeof(T) == 8;
+  const size_t smem = 1024 + 2 * PD::kBytes + 2 * kPair * PT::kBytes + (kInPlaceT ? 0 : kPair * PD::kBytes) + 64;
   cudaError_t e = cudaFuncSetAttribute(tt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int sms = 148;
   device_sm_count(&sms);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tt_kernel<T>, kThreads, smem);
+  const std::int64_t npairs = (L.Nb + kPair - 1) / kPair;
   std::int64_t grid = static_cast<std::int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
-  if (grid > L.Nb) grid = L.Nb;
+  if (grid > npairs) grid = npairs;
   tt_kernel<T><<<static_cast<int>(grid), kThreads, smem, stream>>>(d, tm);
   return cudaGetLastError();
 }

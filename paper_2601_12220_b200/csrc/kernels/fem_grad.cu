@@ -58,12 +58,32 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
   const std::int64_t E = p.E;
   const std::int64_t ntiles = (E + TE - 1) / TE;
 
+  const std::uint64_t pol = ptx::policy_evict_first();
+  auto issue = [&](std::int64_t tile, int s) {
+    const std::int64_t e0 = tile * TE;
+    const int cnt = static_cast<int>(E - e0 < TE ? E - e0 : TE);
+    const std::uint32_t jb = static_cast<std::uint32_t>(cnt) * 8u;
+    const std::uint32_t ub = static_cast<std::uint32_t>(cnt) * NJ * 8u;
+    ptx::mbar_arrive_expect_tx(&full[s], static_cast<std::uint32_t>(p.n_j * NX * NR) * jb +
+                                             static_cast<std::uint32_t>(p.n_u) * ub);
+    double* st = ring + static_cast<size_t>(s) * stage_doubles;
+    for (int a = 0; a < p.n_j; ++a)
+      for (int xr = 0; xr < NX * NR; ++xr)
+        ptx::bulk_g2s_hint(st + a * kJTile + xr * TE, p.J[a] + xr * E + e0, jb, &full[s], pol);
+    double* su = st + p.n_j * kJTile;
+    for (int u = 0; u < p.n_u; ++u) ptx::bulk_g2s_hint(su + u * kUTile, p.U[u] + e0 * NJ, ub, &full[s], pol);
+  };
+  // the producer thread starts the first S tile loads before the CTA-wide
+  // setup below, so their latency overlaps it (matters for small E, e.g. C1)
+  int prefetched = 0;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], kConsumerWarps);
     }
     ptx::fence_barrier_init();
+    for (std::int64_t tile = blockIdx.x; tile < ntiles && prefetched < S; tile += gridDim.x, ++prefetched)
+      issue(tile, prefetched);
   }
   for (int t = tid; t < p.n_d * NX * NI * NJ; t += blockDim.x) {
     const int which = t / (NX * NI * NJ);
@@ -80,26 +100,14 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
 
   if (warp == 0) {
     // ------------------------------ producer ------------------------------
-    if (!ptx::elect_one()) return;
-    const std::uint64_t pol = ptx::policy_evict_first();
+    if (tid != 0) return;
     int it = 0;
     for (std::int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      if (it < prefetched) continue;
       const int s = it % S;
       const std::uint32_t round = static_cast<std::uint32_t>(it / S);
       ptx::mbar_wait(&empty[s], (round & 1u) ^ 1u);
-      const std::int64_t e0 = tile * TE;
-      const int cnt = static_cast<int>(E - e0 < TE ? E - e0 : TE);
-      const std::uint32_t jb = static_cast<std::uint32_t>(cnt) * 8u;
-      const std::uint32_t ub = static_cast<std::uint32_t>(cnt) * NJ * 8u;
-      ptx::mbar_arrive_expect_tx(&full[s], static_cast<std::uint32_t>(p.n_j * NX * NR) * jb +
-                                               static_cast<std::uint32_t>(p.n_u) * ub);
-      double* st = ring + static_cast<size_t>(s) * stage_doubles;
-      for (int a = 0; a < p.n_j; ++a)
-        for (int xr = 0; xr < NX * NR; ++xr)
-          ptx::bulk_g2s_hint(st + a * kJTile + xr * TE, p.J[a] + xr * E + e0, jb, &full[s], pol);
-      double* su = st + p.n_j * kJTile;
-      for (int u = 0; u < p.n_u; ++u)
-        ptx::bulk_g2s_hint(su + u * kUTile, p.U[u] + e0 * NJ, ub, &full[s], pol);
+      issue(tile, s);
     }
     return;
   }
@@ -155,21 +163,18 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
             for (int j = 0; j < NJ; ++j) dreg[x][j] = dq[(x * NI + i) * NJ + j];
         }
         const double* ur = ubase + (kPlainU ? p.row_u_first[q] : q) * urow_stride + el * NJ;
-        // two accumulators per x (even / odd j): 2*NX independent FMA chains
-        double t[NX], t2[NX];
+        double t[NX];
 #pragma unroll
-        for (int x = 0; x < NX; ++x) t[x] = t2[x] = 0.0;
+        for (int x = 0; x < NX; ++x) t[x] = 0.0;
 #pragma unroll
         for (int j = 0; j < NJ; j += 2) {
           const double2 u = *reinterpret_cast<const double2*>(ur + j);
 #pragma unroll
           for (int x = 0; x < NX; ++x) {
             t[x] = fma(dreg[x][j], u.x, t[x]);
-            t2[x] = fma(dreg[x][j + 1], u.y, t2[x]);
+            t[x] = fma(dreg[x][j + 1], u.y, t[x]);
           }
         }
-#pragma unroll
-        for (int x = 0; x < NX; ++x) t[x] += t2[x];
         const double* jt = st + p.row_j[q] * kJTile;
         double* yq = p.Y[q];
 #pragma unroll

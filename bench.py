@@ -165,6 +165,7 @@ class Workload:
             t = torch.empty(m["shape"], dtype=fe._torch_dtype(m["storage"]), device=dev)
             fe.fill_dyadic(t, seed * 1000 + k)
             self.ins.append(t)
+        self.seed = seed
         self.outs = self.plan.alloc_outputs(dev)
         self.launches = 1 + (1 if info.get("operand_flops", 0) and "alpha" in str(payload) else 0)
 
@@ -181,10 +182,15 @@ def gpu_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NCCL over NVLink for the timing barrier / max-reduce / verification
+    # gather; FE_DIST_BACKEND=gloo exercises the multi-rank path on one GPU.
+    backend = os.environ.get("FE_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group(backend, init_method="env://")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
@@ -192,7 +198,7 @@ def gpu_arm(args):
     loads, skipped = [], {}
     for i, n in enumerate(names):
         try:
-            w = Workload(n, rank, world, torch, fe, seed=i + 1)
+            w = Workload(n, rank, world, torch, fe, seed=(i + 1) * 100 + rank)
         except fe.FeinsumError as ex:
             skipped[n] = str(ex)
             continue
@@ -235,7 +241,7 @@ def gpu_arm(args):
     if world > 1:
         dist.barrier()
 
-    mean_t = torch.tensor([sum(t) / len(t) for t in times], dtype=torch.float64, device=dev)
+    mean_t = torch.tensor([sum(t) / len(t) for t in times], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(mean_t, op=dist.ReduceOp.MAX)
     mean_t = mean_t.cpu().tolist()
@@ -254,8 +260,14 @@ def gpu_arm(args):
         agg_flops = w.global_flops  # the global (world x config) problem, one shard per rank
         gflops = agg_flops / t / 1e9
         rates.append(gflops)
+        # per-config roofline: slower of HBM (footprint bytes) and FP64 (DMMA
+        # peak for the DMMA kernels, DFMA peak for the DFMA kernels)
+        fp_peak = fp64.get("dmma" if w.transform in ("gett_dmma/v1", "tt/v1") else "dfma", 0.0) * 1e12
+        roof_t = max(w.bytes / (peaks["hbm_gbs"] * 1e9), w.flops / fp_peak if fp_peak else 0.0)
         per[w.name] = {"ms": t * 1e3, "gflops": gflops, "gbs": w.bytes * world / t / 1e9,
-                       "transform": w.transform, "source": w.source, "flops": w.flops, "bytes": w.bytes}
+                       "transform": w.transform, "source": w.source, "flops": w.flops, "bytes": w.bytes,
+                       "roof_ms": roof_t * 1e3, "roof_frac": roof_t / t,
+                       "bound": "hbm" if w.bytes / (peaks["hbm_gbs"] * 1e9) >= roof_t else "fp64"}
     value = math.exp(sum(math.log(r) for r in rates) / len(rates)) if rates else 0.0
     ms_step = sum(mean_t) * 1e3
 
@@ -264,22 +276,29 @@ def gpu_arm(args):
     roof = None
     if dom is not None:
         w, t = loads[dom], mean_t[dom]
-        fp64_peak = max(fp64.values()) if fp64 else None
+        pipe = "dmma" if w.transform in ("gett_dmma/v1", "tt/v1") else "dfma"
+        fp64_peak = fp64.get(pipe)
         hbm_time = w.bytes / (peaks["hbm_gbs"] * 1e9)
         fp_time = w.flops / (fp64_peak * 1e12) if fp64_peak else 0
         if hbm_time >= fp_time:
             roof = {"bound": "hbm", "achieved": w.bytes / t / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs)"}
         else:
-            roof = {"bound": "tensor", "achieved": w.flops / t / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
-                    "peak_source": "measured on this GPU by fe_fp64_peak (FP64 %s)" % max(fp64, key=fp64.get)}
+            # FP64 work: tcgen05 has no f64 kind, so the denominator is the FP64
+            # pipe this kernel issues to (DMMA tensor cores or DFMA), measured
+            # on this GPU; MEASURED_PEAKS.json only carries HBM and bf16
+            roof = {"bound": "tensor" if pipe == "dmma" else "fp64", "achieved": w.flops / t / 1e12,
+                    "peak": fp64_peak, "unit": "TFLOP/s",
+                    "peak_source": "measured on this GPU by fe_fp64_peak (FP64 %s)" % pipe.upper()}
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["kernel"] = w.name + ":" + w.transform
         roof["traffic"] = None
 
+    verify = verify_shards(loads, torch, fe, rank, world, dist, cdev) if world > 1 else None
+
     e2e = None
     if not args.no_e2e and loads:
-        e2e = e2e_pass(args, loads, torch, fe, world, dist if world > 1 else None)
+        e2e = e2e_pass(args, loads, torch, fe, world, dist if world > 1 else None, cdev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -300,12 +319,44 @@ def gpu_arm(args):
             "gpu_launches": args.steps * sum(1 + w.launches for w in loads),
             "e2e": e2e, "cpu_baseline": cpu,
         }
+        if verify is not None:
+            line["verify"] = verify
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 
 
-def e2e_pass(args, loads, torch, fe, world, dist):
+def verify_shards(loads, torch, fe, rank, world, dist, cdev):
+    """Verification gather (outside the timed region): every rank's shard was
+    filled from its own seeds; each rank sends per-output checksums (sum and
+    sum of squares, fp64) to all ranks, and rank 0 recomputes every other
+    rank's shard on its own GPU from the same seeds and compares."""
+    report = {}
+    for k, w in enumerate(loads):
+        mine = torch.tensor([float(o.double().sum()) for o in w.outs] + [float(o.double().pow(2).sum()) for o in w.outs],
+                            dtype=torch.float64, device=cdev)
+        got = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(got, mine)
+        ok = True
+        if rank == 0:
+            seed_base = w.seed - rank
+            for r in range(1, world):
+                ins = []
+                for j, m in enumerate(w.plan.inputs):
+                    t = torch.empty(m["shape"], dtype=fe._torch_dtype(m["storage"]), device="cuda")
+                    fe.fill_dyadic(t, (seed_base + r) * 1000 + j)
+                    ins.append(t)
+                outs = w.plan(*ins)
+                ref = torch.tensor([float(o.double().sum()) for o in outs] + [float(o.double().pow(2).sum()) for o in outs],
+                                   dtype=torch.float64)
+                ok = ok and torch.allclose(ref, got[r].cpu(), rtol=1e-12, atol=1e-9)
+                del ins, outs
+            report[w.name] = bool(ok)
+    return {"ok": all(report.values()), "per_config": report,
+            "method": "all_gather of per-shard output checksums; rank 0 recomputes each shard from its seeds"}
+
+
+def e2e_pass(args, loads, torch, fe, world, dist, cdev=None):
     """Same metric through the C-ABI with pinned HOST buffers: H2D of the
     inputs, kernels, D2H of the outputs, all inside the timed region."""
     stream = torch.cuda.current_stream()
@@ -330,7 +381,7 @@ def e2e_pass(args, loads, torch, fe, world, dist):
             tot += t0.elapsed_time(t1) * 1e-3
         t = tot / steps
         if dist is not None:
-            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([t], dtype=torch.float64, device=cdev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t = tt.item()
         rates.append(w.flops * world / t / 1e9)

@@ -1160,6 +1160,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
     L.NI = f.NI;
     L.NJ = f.NJ;
     L.stages = meta_int(plan.meta, "stages", 4);
+    L.d_in_smem = meta_int(plan.meta, "dsmem", 0) != 0;
     std::vector<int> jl, dl;
     bool ok = true;
     int u = 0;

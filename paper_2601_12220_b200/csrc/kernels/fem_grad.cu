@@ -33,8 +33,11 @@ struct Coef {
   int sign;
 };
 
-template <int NX, int NR, int NI, int NJ, int TE, bool kPlainU>
-__global__ void __launch_bounds__(32 + TE * NI, 1)
+// kDSmem: read D from shared memory (broadcast LDS.128) instead of holding
+// D[x,i,:] in 60 registers — halves the register footprint so two CTAs fit
+// per SM (more warps in flight for the HBM-bound loop); chosen per fact meta.
+template <int NX, int NR, int NI, int NJ, int TE, bool kPlainU, bool kDSmem>
+__global__ void __launch_bounds__(32 + TE * NI, kDSmem ? 2 : 1)
     fem_grad_kernel(const __grid_constant__ FemGradLaunch p) {
   constexpr int kConsumers = TE * NI;
   static_assert(kConsumers % 32 == 0, "consumer threads must fill warps");
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
   const int c = tid - 32;
   const int el = c / NI;
   const int i = c - el * NI;
-  double dreg[NX][NJ];
+  double dreg[kDSmem ? 1 : NX][kDSmem ? 2 : NJ];
   int cur_d = -1;
   int it = 0;
   for (std::int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -154,7 +157,8 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
 
     if (e0 + el < E) {
       for (int q = 0; q < p.rows; ++q) {
-        if (p.row_d[q] != cur_d) {
+        const double* dq_row = dsm + p.row_d[q] * NX * NI * NJ + i * NJ;  // D_q[x][i][:] at x*NI*NJ
+        if (!kDSmem && p.row_d[q] != cur_d) {
           cur_d = p.row_d[q];
           const double* dq = dsm + cur_d * NX * NI * NJ;
 #pragma unroll
@@ -162,6 +166,7 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
 #pragma unroll
             for (int j = 0; j < NJ; ++j) dreg[x][j] = dq[(x * NI + i) * NJ + j];
         }
+        (void)dq_row;
         const double* ur = ubase + (kPlainU ? p.row_u_first[q] : q) * urow_stride + el * NJ;
         double t[NX];
 #pragma unroll
@@ -171,8 +176,14 @@ __global__ void __launch_bounds__(32 + TE * NI, 1)
           const double2 u = *reinterpret_cast<const double2*>(ur + j);
 #pragma unroll
           for (int x = 0; x < NX; ++x) {
-            t[x] = fma(dreg[x][j], u.x, t[x]);
-            t[x] = fma(dreg[x][j + 1], u.y, t[x]);
+            if constexpr (kDSmem) {
+              const double2 dd = *reinterpret_cast<const double2*>(dq_row + x * NI * NJ + j);
+              t[x] = fma(dd.x, u.x, t[x]);
+              t[x] = fma(dd.y, u.y, t[x]);
+            } else {
+              t[x] = fma(dreg[x][j], u.x, t[x]);
+              t[x] = fma(dreg[x][j + 1], u.y, t[x]);
+            }
           }
         }
         const double* jt = st + p.row_j[q] * kJTile;
@@ -211,8 +222,12 @@ int launch_shape(const FemGradLaunch& p, cudaStream_t s) {
     kern<<<static_cast<int>(grid), 32 + TE * NI, smem, s>>>(p);
     return cudaGetLastError();
   };
-  if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true>);
-  return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false>);
+  if (p.d_in_smem) {
+    if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, true>);
+    return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, true>);
+  }
+  if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, false>);
+  return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, false>);
 }
 
 }  // namespace

@@ -179,6 +179,7 @@ struct FemGradLaunch {
   int u_sign[kFemMaxUTiles], u_pre[kFemMaxUTiles], u_post[kFemMaxUTiles];
   int row_u_first[kFemMaxRows], row_u_count[kFemMaxRows];
   bool plain_u;        // every row: one term, no coefficients
+  bool d_in_smem;      // D read from shared memory (2 CTAs/SM) instead of registers
   const double* coef;  // interleaved complex coefficients (real part used)
   double* Y[kFemMaxRows];
 };

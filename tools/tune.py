@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 CANDIDATES = {
-    "fem_grad/v1": ["stages=2", "stages=3", "stages=4", "stages=6"],
+    "fem_grad/v1": ["stages=2", "stages=4", "stages=6", "stages=2;dsmem=1", "stages=3;dsmem=1", "stages=4;dsmem=1"],
     "gett_dmma/v1": ["stages=2;group=12", "stages=3;group=6", "stages=3;group=12", "stages=3;group=24"],
     "tt/v1": ["stages=2"],
     "hex_sumfact/v1": [""],

@@ -120,41 +120,51 @@ __device__ __forceinline__ void cols5(double (&v)[P][P], const double (&c)[MS]) 
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) hex_kernel(const __grid_constant__ HexDev p) {
+__global__ void __launch_bounds__(kThreads, 2) hex_kernel(const __grid_constant__ HexDev p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);
   const int R = p.rows;
   const int nblk = NE * R;  // (element, field) cubes per pair
-  // layout (doubles): ops[6][ND][MS] | stage[2] {G: 9*NE*P3, U: R*NE*P3} | WA[ND][nblk][CB] | WB[ND][nblk][CB]
+  // layout (doubles): ops[6][ND][MS] | Gs[9][NE*P3] | Us[R][NE*P3] | W[ND][nblk][CB] | mbar {G, U}
   double* ops = sm;
-  double* stage0 = ops + 6 * ND * MS;
-  const int g_len = ND * ND * NE * P3, stage_len = g_len + R * NE * P3;
-  double* WA = stage0 + 2 * stage_len;
-  double* WB = WA + ND * nblk * CB;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(WB + ND * nblk * CB);
+  double* Gs = ops + 6 * ND * MS;
+  const int g_len = ND * ND * NE * P3;
+  double* Us = Gs + g_len;
+  double* W = Us + R * NE * P3;
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(W + ND * nblk * CB);
 
   for (int t = threadIdx.x; t < 6 * ND * MS; t += blockDim.x) {
     const int k = t / (ND * MS), d = (t / MS) % ND, e = t % MS;
     ops[t] = e < P2 ? __ldg(p.mats[k] + d * P2 + e) : 0.0;
   }
   if (threadIdx.x == 0) {
-    ptx::mbar_init(&full[0], 1);
-    ptx::mbar_init(&full[1], 1);
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
     ptx::fence_barrier_init();
   }
   __syncthreads();
 
   const std::int64_t npairs = p.E / NE;
   const std::uint32_t bytes = static_cast<std::uint32_t>(NE * P3 * 8);
-  auto issue = [&](std::int64_t pair, int s) {
-    double* st = stage0 + s * stage_len;
-    ptx::mbar_arrive_expect_tx(&full[s], bytes * static_cast<std::uint32_t>(ND * ND + R));
+  // G and U have separate single-buffered slots: each is refilled for the
+  // next pair as soon as the pass that consumes it is done (U after pass 1,
+  // G after the combine), so the copies overlap the remaining passes and the
+  // second CTA on the SM covers what is left.
+  auto issue_g = [&](std::int64_t pair) {
+    ptx::mbar_arrive_expect_tx(&bar[0], bytes * static_cast<std::uint32_t>(ND * ND));
     const std::int64_t e0 = pair * NE;
     for (int xy = 0; xy < ND * ND; ++xy)
-      ptx::bulk_g2s(st + xy * NE * P3, p.G + (xy * p.E + e0) * P3, bytes, &full[s]);
-    for (int f = 0; f < R; ++f) ptx::bulk_g2s(st + g_len + f * NE * P3, p.U[f] + e0 * P3, bytes, &full[s]);
+      ptx::bulk_g2s(Gs + xy * NE * P3, p.G + (xy * p.E + e0) * P3, bytes, &bar[0]);
   };
-  if (threadIdx.x == 0 && blockIdx.x < npairs) issue(blockIdx.x, 0);
+  auto issue_u = [&](std::int64_t pair) {
+    ptx::mbar_arrive_expect_tx(&bar[1], bytes * static_cast<std::uint32_t>(R));
+    const std::int64_t e0 = pair * NE;
+    for (int f = 0; f < R; ++f) ptx::bulk_g2s(Us + f * NE * P3, p.U[f] + e0 * P3, bytes, &bar[1]);
+  };
+  if (threadIdx.x == 0 && blockIdx.x < npairs) {
+    issue_u(blockIdx.x);
+    issue_g(blockIdx.x);
+  }
 
   // plane task: direction d, plane index pl, cube blk = el*R + f (cube fastest)
   const int ntask = ND * P * nblk;
@@ -170,20 +180,19 @@ __global__ void __launch_bounds__(kThreads, 1) hex_kernel(const __grid_constant_
   const double* opB1 = ops + (3 * ND + d) * MS;
   const double* opB2 = ops + (4 * ND + d) * MS;
   const double* opB3 = ops + (5 * ND + d) * MS;
+  double* cube = W + (d * nblk + blk) * CB;  // this task's direction cube
 
   int it = 0;
   for (std::int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x, ++it) {
-    const int s = it & 1;
-    ptx::mbar_wait(&full[s], static_cast<std::uint32_t>((it >> 1) & 1));
-    if (threadIdx.x == 0 && pair + gridDim.x < npairs) issue(pair + gridDim.x, s ^ 1);
-    const double* G = stage0 + s * stage_len;  // [x*3+y][el][125]
-    const double* U = G + g_len;               // [f][el][125]
+    const std::uint32_t phase = static_cast<std::uint32_t>(it & 1);
+    const bool more = pair + gridDim.x < npairs;
     double v[P][P];
     double c[MS];
 
     // pass 1 (direction y = d, plane j = pl): F3 along l, F2 along k
+    ptx::mbar_wait(&bar[1], phase);
     if (active) {
-      const double* in = U + (f * NE + el) * P3 + pl * P2;
+      const double* in = Us + (f * NE + el) * P3 + pl * P2;
 #pragma unroll
       for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -192,32 +201,33 @@ __global__ void __launch_bounds__(kThreads, 1) hex_kernel(const __grid_constant_
       rows5<false>(v, c);
       load_op(opF2, c);
       cols5<false>(v, c);
-      double* out = WA + (d * nblk + blk) * CB + pl * PL;  // [j][b][c]
+      double* out = cube + pl * PL;  // [j][b][c]
 #pragma unroll
       for (int b = 0; b < P; ++b) store_row(out + b * RW, v[b]);
     }
     __syncthreads();
-    // pass 2 (direction y = d, plane b = pl): F1 along j -> t_y[a][b][c]
+    if (threadIdx.x == 0 && more) issue_u(pair + gridDim.x);
+    // pass 2 (direction y = d, plane b = pl), in place: F1 along j -> t_y[a][b][c]
     if (active) {
-      const double* in = WA + (d * nblk + blk) * CB + pl * RW;
+      double* io = cube + pl * RW;
 #pragma unroll
-      for (int j = 0; j < P; ++j) load_row(in + j * PL, v[j]);
+      for (int j = 0; j < P; ++j) load_row(io + j * PL, v[j]);
       load_op(opF1, c);
       cols5<false>(v, c);
-      double* out = WB + (d * nblk + blk) * CB + pl * RW;
 #pragma unroll
-      for (int a = 0; a < P; ++a) store_row(out + a * PL, v[a]);
+      for (int a = 0; a < P; ++a) store_row(io + a * PL, v[a]);
     }
     __syncthreads();
-    // pass 3 (direction x = d, plane b = pl): q_x = sum_y G[x,y] t_y, B1^T along a -> i
+    // pass 3a (direction x = d, plane b = pl): q_x = sum_y G[x,y] t_y into registers
+    ptx::mbar_wait(&bar[0], phase);
     if (active) {
-      const double* g = G + (d * ND * NE + el) * P3 + pl * P;
+      const double* g = Gs + (d * ND * NE + el) * P3 + pl * P;
 #pragma unroll
       for (int a = 0; a < P; ++a) {
         double t0[P], t1[P], t2[P];
-        load_row(WB + (0 * nblk + blk) * CB + a * PL + pl * RW, t0);
-        load_row(WB + (1 * nblk + blk) * CB + a * PL + pl * RW, t1);
-        load_row(WB + (2 * nblk + blk) * CB + a * PL + pl * RW, t2);
+        load_row(W + (0 * nblk + blk) * CB + a * PL + pl * RW, t0);
+        load_row(W + (1 * nblk + blk) * CB + a * PL + pl * RW, t1);
+        load_row(W + (2 * nblk + blk) * CB + a * PL + pl * RW, t2);
 #pragma unroll
         for (int cc = 0; cc < P; ++cc) {
           double q = g[a * P2 + cc] * t0[cc];
@@ -225,37 +235,48 @@ __global__ void __launch_bounds__(kThreads, 1) hex_kernel(const __grid_constant_
           v[a][cc] = fma(g[2 * NE * P3 + a * P2 + cc], t2[cc], q);
         }
       }
+    }
+    __syncthreads();  // every t_y and G read
+    if (threadIdx.x == 0 && more) issue_g(pair + gridDim.x);
+    // pass 3b, in place: B1^T along a -> i
+    if (active) {
       load_op(opB1, c);
       cols5<true>(v, c);
-      double* out = WA + (d * nblk + blk) * CB + pl * RW;  // [i][b][c]
+      double* out = cube + pl * RW;  // [i][b][c]
 #pragma unroll
       for (int i = 0; i < P; ++i) store_row(out + i * PL, v[i]);
     }
     __syncthreads();
-    // pass 4 (direction x = d, plane i = pl): B2^T along b -> m, B3^T along c -> n
+    // pass 4 (direction x = d, plane i = pl), in place: B2^T along b -> m, B3^T along c -> n
     if (active) {
-      const double* in = WA + (d * nblk + blk) * CB + pl * PL;
+      double* io = cube + pl * PL;
 #pragma unroll
-      for (int b = 0; b < P; ++b) load_row(in + b * RW, v[b]);
+      for (int b = 0; b < P; ++b) load_row(io + b * RW, v[b]);
       load_op(opB2, c);
       cols5<true>(v, c);
       load_op(opB3, c);
       rows5<true>(v, c);
-      double* out = WB + (d * nblk + blk) * CB + pl * PL;  // partial y_x[i][m][n]
 #pragma unroll
-      for (int m = 0; m < P; ++m) store_row(out + m * RW, v[m]);
+      for (int m = 0; m < P; ++m) store_row(io + m * RW, v[m]);  // partial y_x[i][m][n]
     }
     __syncthreads();
-    // sum the three direction partials; consecutive threads write consecutive
-    // doubles of one field's 250-double pair run
+    // sum the three direction partials row by row (one padded row of 5 per
+    // task, vector shared loads, no per-point index arithmetic); consecutive
+    // tasks write consecutive rows of one cube
     const std::int64_t e0 = pair * NE;
-    for (int t = threadIdx.x; t < nblk * P3; t += blockDim.x) {
-      const int ff = t / (NE * P3), rem = t % (NE * P3);
-      const int ee = rem / P3, pt = rem % P3;
-      const int off = (ee * R + ff) * CB + (pt / P2) * PL + ((pt / P) % P) * RW + pt % P;
-      const double y = WB[off] + WB[nblk * CB + off] + WB[2 * nblk * CB + off];
-      __stcs(p.Y[ff] + e0 * P3 + rem, y);
+    for (int t = threadIdx.x; t < nblk * P2; t += blockDim.x) {
+      const int b2 = t / P2, row = t - b2 * P2;  // row = i*5 + m
+      const int off = b2 * CB + (row / P) * PL + (row % P) * RW;
+      double r0[P], r1[P], r2[P];
+      load_row(W + off, r0);
+      load_row(W + nblk * CB + off, r1);
+      load_row(W + 2 * nblk * CB + off, r2);
+      const int ee = b2 / R, ff = b2 - ee * R;
+      double* y = p.Y[ff] + (e0 + ee) * P3 + row * P;
+#pragma unroll
+      for (int n = 0; n < P; ++n) __stcs(y + n, r0[n] + r1[n] + r2[n]);
     }
+    __syncthreads();  // W is rewritten by the next pair's pass 1
   }
 }
 
@@ -278,7 +299,7 @@ int launch_hex(const HexLaunch& L, void* stream) {
   }
   for (int k = 0; k < 6; ++k) d.mats[k] = L.mats[k];
   const int R = L.rows;
-  const size_t doubles = 6 * ND * MS + 2 * (ND * ND * NE * P3 + R * NE * P3) + 2 * ND * NE * R * CB;
+  const size_t doubles = 6 * ND * MS + ND * ND * NE * P3 + R * NE * P3 + ND * NE * R * CB;
   const size_t smem = doubles * 8 + 16;
   cudaError_t e = cudaFuncSetAttribute(hex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

@@ -1196,10 +1196,15 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
     }
     for (size_t a = 0; a < dl.size(); ++a) L.D[a] = static_cast<const double*>(d_in[dl[a]]);
     L.coef = plan.d_coef;
-    L.tile_e = f.NI == 10 ? 32 : (f.NI == 4 ? 64 : 16);
+    L.tile_e = meta_int(plan.meta, "te", f.NI == 10 ? 32 : (f.NI == 4 ? 64 : 16));
     L.grid = meta_int(plan.meta, "grid", 0);  // 0: all resident CTAs
+    L.ept = meta_int(plan.meta, "ept", 1);
+    L.mma = meta_int(plan.meta, "mma", 0) != 0 && fem_mma_supported(L.NX, L.NR, L.NI, L.NJ);
     if (ok) {
-      cuda_check(launch_fem_grad(L, stream), "fem_grad kernel");
+      if (L.mma)
+        cuda_check(launch_fem_mma(L, stream), "fem_mma kernel");
+      else
+        cuda_check(launch_fem_grad(L, stream), "fem_grad kernel");
       return;
     }
   }

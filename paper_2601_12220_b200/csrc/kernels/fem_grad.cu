@@ -36,10 +36,13 @@ struct Coef {
 // kDSmem: read D from shared memory (broadcast LDS.128) instead of holding
 // D[x,i,:] in 60 registers — halves the register footprint so two CTAs fit
 // per SM (more warps in flight for the HBM-bound loop); chosen per fact meta.
-template <int NX, int NR, int NI, int NJ, int TE, bool kPlainU, bool kDSmem>
-__global__ void __launch_bounds__(32 + TE * NI, kDSmem ? 2 : 1)
+// EPT: elements per consumer thread (el, el + TE/EPT, ...): more independent
+// FMA chains per thread and D reused from registers across them.
+template <int NX, int NR, int NI, int NJ, int TE, bool kPlainU, bool kDSmem, int EPT = 1>
+__global__ void __launch_bounds__(32 + TE * NI / EPT, kDSmem ? 2 : 1)
     fem_grad_kernel(const __grid_constant__ FemGradLaunch p) {
-  constexpr int kConsumers = TE * NI;
+  constexpr int kConsumers = TE * NI / EPT;
+  constexpr int kES = TE / EPT;  // element stride between a thread's elements
   static_assert(kConsumers % 32 == 0, "consumer threads must fill warps");
   constexpr int kConsumerWarps = kConsumers / 32;
   static_assert(NJ % 2 == 0, "U rows are read as double2");
@@ -138,16 +141,37 @@ __global__ void __launch_bounds__(32 + TE * NI, kDSmem ? 2 : 1)
       urow_stride = kUTile;  // row q reads leaf tile row_u_first[q] == q
     } else {
       double* uc = ucomb + (it & 1) * p.rows * kUTile;
+      // (pre * leaf) * post per term, terms accumulated left to right — the
+      // operand's own order; two values per thread and iteration (16-byte
+      // shared accesses), the two-term form a*x +- b*y with its coefficients
+      // in registers
+      auto term = [](const Coef& cf, double v) { return __dmul_rn(__dmul_rn(cf.pre, v), cf.post); };
+      auto join = [](const Coef& cf, double acc, double x) {
+        return cf.sign > 0 ? __dadd_rn(acc, x) : __dsub_rn(acc, x);
+      };
       for (int q = 0; q < p.rows; ++q) {
         const int u0 = p.row_u_first[q], nt = p.row_u_count[q];
-        for (int v = c; v < kUTile; v += kConsumers) {
-          double acc = 0.0;
-          for (int k = 0; k < nt; ++k) {
-            const Coef cf = coefs[u0 + k];
-            const double x = __dmul_rn(__dmul_rn(cf.pre, su[(u0 + k) * kUTile + v]), cf.post);
-            acc = k == 0 ? x : (cf.sign > 0 ? __dadd_rn(acc, x) : __dsub_rn(acc, x));
+        const double2* s0 = reinterpret_cast<const double2*>(su + u0 * kUTile);
+        double2* o = reinterpret_cast<double2*>(uc + q * kUTile);
+        if (nt == 2) {
+          const Coef c0 = coefs[u0], c1 = coefs[u0 + 1];
+          const double2* s1 = s0 + kUTile / 2;
+          for (int v = c; v < kUTile / 2; v += kConsumers) {
+            const double2 a = s0[v], b = s1[v];
+            o[v] = make_double2(join(c1, term(c0, a.x), term(c1, b.x)), join(c1, term(c0, a.y), term(c1, b.y)));
           }
-          uc[q * kUTile + v] = acc;
+        } else {
+          for (int v = c; v < kUTile / 2; v += kConsumers) {
+            const Coef c0 = coefs[u0];
+            const double2 a = s0[v];
+            double2 acc = make_double2(term(c0, a.x), term(c0, a.y));
+            for (int k = 1; k < nt; ++k) {
+              const Coef ck = coefs[u0 + k];
+              const double2 b = s0[k * (kUTile / 2) + v];
+              acc = make_double2(join(ck, acc.x, term(ck, b.x)), join(ck, acc.y, term(ck, b.y)));
+            }
+            o[v] = acc;
+          }
         }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
@@ -168,21 +192,31 @@ __global__ void __launch_bounds__(32 + TE * NI, kDSmem ? 2 : 1)
         }
         (void)dq_row;
         const double* ur = ubase + (kPlainU ? p.row_u_first[q] : q) * urow_stride + el * NJ;
-        double t[NX];
+        double t[EPT][NX];
 #pragma unroll
-        for (int x = 0; x < NX; ++x) t[x] = 0.0;
+        for (int h = 0; h < EPT; ++h)
+#pragma unroll
+          for (int x = 0; x < NX; ++x) t[h][x] = 0.0;
 #pragma unroll
         for (int j = 0; j < NJ; j += 2) {
-          const double2 u = *reinterpret_cast<const double2*>(ur + j);
+          double2 u[EPT];
+#pragma unroll
+          for (int h = 0; h < EPT; ++h) u[h] = *reinterpret_cast<const double2*>(ur + h * kES * NJ + j);
 #pragma unroll
           for (int x = 0; x < NX; ++x) {
+            double d0, d1;
             if constexpr (kDSmem) {
               const double2 dd = *reinterpret_cast<const double2*>(dq_row + x * NI * NJ + j);
-              t[x] = fma(dd.x, u.x, t[x]);
-              t[x] = fma(dd.y, u.y, t[x]);
+              d0 = dd.x;
+              d1 = dd.y;
             } else {
-              t[x] = fma(dreg[x][j], u.x, t[x]);
-              t[x] = fma(dreg[x][j + 1], u.y, t[x]);
+              d0 = dreg[x][j];
+              d1 = dreg[x][j + 1];
+            }
+#pragma unroll
+            for (int h = 0; h < EPT; ++h) {
+              t[h][x] = fma(d0, u[h].x, t[h][x]);
+              t[h][x] = fma(d1, u[h].y, t[h][x]);
             }
           }
         }
@@ -190,10 +224,14 @@ __global__ void __launch_bounds__(32 + TE * NI, kDSmem ? 2 : 1)
         double* yq = p.Y[q];
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
-          double y = 0.0;
 #pragma unroll
-          for (int x = 0; x < NX; ++x) y = fma(jt[(x * NR + r) * TE + el], t[x], y);
-          __stcs(yq + (static_cast<std::int64_t>(r) * E + e0 + el) * NI + i, y);
+          for (int h = 0; h < EPT; ++h) {
+            double y = 0.0;
+#pragma unroll
+            for (int x = 0; x < NX; ++x) y = fma(jt[(x * NR + r) * TE + el + h * kES], t[h][x], y);
+            if (h == 0 || e0 + el + h * kES < E)
+              __stcs(yq + (static_cast<std::int64_t>(r) * E + e0 + el + h * kES) * NI + i, y);
+          }
         }
       }
     }
@@ -202,8 +240,9 @@ __global__ void __launch_bounds__(32 + TE * NI, kDSmem ? 2 : 1)
   }
 }
 
-template <int NX, int NR, int NI, int NJ, int TE>
+template <int NX, int NR, int NI, int NJ, int TE, int EPT = 1>
 int launch_shape(const FemGradLaunch& p, cudaStream_t s) {
+  constexpr int kThreads = 32 + TE * NI / EPT;
   const bool plain = p.plain_u;
   const size_t doubles = static_cast<size_t>(p.n_d) * NX * NI * NJ +
                          static_cast<size_t>(p.stages) * (p.n_j * NX * NR * TE + p.n_u * TE * NJ) +
@@ -214,20 +253,25 @@ int launch_shape(const FemGradLaunch& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     int sms = 148, per_sm = 1;
     device_sm_count(&sms);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 + TE * NI, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
     const std::int64_t ntiles = (p.E + TE - 1) / TE;
     std::int64_t grid = static_cast<std::int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
     if (p.grid > 0) grid = p.grid;
     if (grid > ntiles) grid = ntiles;
-    kern<<<static_cast<int>(grid), 32 + TE * NI, smem, s>>>(p);
+    kern<<<static_cast<int>(grid), kThreads, smem, s>>>(p);
     return cudaGetLastError();
   };
-  if (p.d_in_smem) {
-    if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, true>);
-    return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, true>);
+  if constexpr (EPT > 1) {
+    if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, false, EPT>);
+    return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, false, EPT>);
+  } else {
+    if (p.d_in_smem) {
+      if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, true>);
+      return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, true>);
+    }
+    if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, false>);
+    return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, false>);
   }
-  if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, false>);
-  return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, false>);
 }
 
 }  // namespace
@@ -239,7 +283,12 @@ bool fem_grad_supported(int NX, int NR, int NI, int NJ) {
 int launch_fem_grad(const FemGradLaunch& p, void* stream) {
   if (p.E == 0) return cudaSuccess;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (p.NI == 10 && p.NJ == 10) return launch_shape<3, 3, 10, 10, 32>(p, s);
+  if (p.NI == 10 && p.NJ == 10) {
+    // small batches: half-size tiles put more CTAs in flight (latency-bound)
+    if (p.tile_e == 16) return launch_shape<3, 3, 10, 10, 16>(p, s);
+    if (p.ept == 2) return launch_shape<3, 3, 10, 10, 32, 2>(p, s);
+    return launch_shape<3, 3, 10, 10, 32>(p, s);
+  }
   if (p.NI == 4 && p.NJ == 4) return launch_shape<3, 3, 4, 4, 64>(p, s);
   if (p.NI == 20 && p.NJ == 20) return launch_shape<3, 3, 20, 20, 16>(p, s);
   return cudaErrorInvalidValue;

@@ -180,12 +180,16 @@ struct FemGradLaunch {
   int row_u_first[kFemMaxRows], row_u_count[kFemMaxRows];
   bool plain_u;        // every row: one term, no coefficients
   bool d_in_smem;      // D read from shared memory (2 CTAs/SM) instead of registers
+  bool mma;            // fem_mma.cu: inner contraction on DMMA (fp64 tensor cores)
+  int ept;             // elements per consumer thread (1 or 2)
   const double* coef;  // interleaved complex coefficients (real part used)
   double* Y[kFemMaxRows];
 };
 
 int launch_fem_grad(const FemGradLaunch& p, void* stream);
 bool fem_grad_supported(int NX, int NR, int NI, int NJ);
+int launch_fem_mma(const FemGradLaunch& p, void* stream);
+bool fem_mma_supported(int NX, int NR, int NI, int NJ);
 
 // evaluate coefficient chains into coef (interleaved complex)
 int launch_coef(const CoefChain* chains, int n_chains, const LeafTable& leaves, double* coef, void* stream);

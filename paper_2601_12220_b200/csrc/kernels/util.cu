@@ -3,6 +3,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "launch.h"
 
 namespace feb200 {
@@ -118,6 +120,13 @@ int fill_dyadic(void* ptr, int storage, std::int64_t count, std::uint64_t seed, 
 
 int flush_l2(void* scratch, std::int64_t bytes, void* stream) {
   static int salt = 0;
+  static const bool carve = [] {
+    const char* v = std::getenv("FE_FLUSH_CARVEOUT");
+    if (v && v[0] == '1')
+      cudaFuncSetAttribute(flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    return true;
+  }();
+  (void)carve;
   int sms = 148;
   device_sm_count(&sms);
   flush_kernel<<<sms * 4, 512, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<int4*>(scratch), bytes / 16, ++salt);

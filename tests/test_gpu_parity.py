@@ -149,6 +149,32 @@ def test_fem_grad_odd_sizes(fe, ref, torch_cuda):
         assert np.array_equal(g, w.real)
 
 
+FEM_VARIANTS = ["stages=2", "stages=4;te=16", "stages=3;dsmem=1", "stages=4;ept=2", "mma=1;stages=4", "mma=1;stages=2;te=16",
+                "mma=1;stages=3;te=64"]
+
+
+@pytest.mark.parametrize("meta", FEM_VARIANTS)
+def test_fem_grad_variants(fe, ref, torch_cuda, meta):
+    """Every tuned K1 variant (DFMA, D in smem, half tiles, DMMA) on ragged
+    tails, several rows, and the C5 functional operands."""
+    from paper_2601_12220_b200 import configs as C
+    opts = {"meta": meta, "transform": "fem_grad/v1"}
+    for E, nb in [(2, 1), (34, 2), (1002, 5), (66, 3), (10_000, 3)]:
+        e = C.fem_grad(E=E, b=nb)
+        plan = fe.Plan(einsum=e, options=opts)
+        assert plan.info["transform"] == "fem_grad/v1" and plan.info["meta"] == meta
+        bind = ref.random_bindings(e, E + 1)
+        for g, w in zip(run_plan(torch_cuda, plan, bind), ref.evaluate(e, bind)):
+            assert rel_err(g, w) <= FP64_TOL, (meta, E)
+    fk = C.wave_kernel(E=4_002)
+    info, arrays, b = _kernel_bindings(ref, fk, 13)
+    plan = fe.Plan(kernel=fk, options=opts)
+    got = run_plan(torch_cuda, plan, b)
+    want = ref.eval_kernel(fk, arrays, b, 3, [3, 4_002, 10])
+    for g, w in zip(got, want):
+        assert rel_err(g, w) <= FP64_TOL, meta
+
+
 def _kernel_bindings(ref, fk, seed):
     info = ref.raise_kernel(fk)
     import re

@@ -16,7 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 CANDIDATES = {
-    "fem_grad/v1": ["stages=2", "stages=4", "stages=6", "stages=2;dsmem=1", "stages=3;dsmem=1", "stages=4;dsmem=1"],
+    "fem_grad/v1": ["stages=4", "stages=2;te=16", "stages=4;te=16", "stages=8;te=16", "stages=3;dsmem=1",
+                    "stages=2;ept=2", "stages=3;ept=2", "stages=4;ept=2", "mma=1;stages=4"],
     "gett_dmma/v1": ["stages=2;group=12", "stages=3;group=6", "stages=3;group=12", "stages=3;group=24"],
     "tt/v1": ["stages=2"],
     "hex_sumfact/v1": [""],

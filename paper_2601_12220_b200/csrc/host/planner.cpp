@@ -1289,7 +1289,10 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         L.x_sn = static_cast<std::int64_t>(b.NJ) * b.NL;
         L.y_sn = static_cast<std::int64_t>(b.NI) * b.NK;
         L.stages = meta_int(plan.meta, "stages", 2);
-        cuda_check(launch_tt(L, stream), "tt kernel");
+        if (L.fp32 && meta_int(plan.meta, "tc", 1) != 0 && tt_tc_supported(L))
+          cuda_check(launch_tt_tc(L, stream), "tt tcgen05 kernel");
+        else
+          cuda_check(launch_tt(L, stream), "tt kernel");
       }
       return;
     }

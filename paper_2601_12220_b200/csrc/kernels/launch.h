@@ -232,6 +232,9 @@ struct TTLaunch {
 
 int launch_tt(const TTLaunch& p, void* stream);
 bool tt_supported(int NI, int NJ, int NK, int NL);
+// fp32 on the tcgen05 tensor cores (3xTF32), tt_tc.cu
+int launch_tt_tc(const TTLaunch& p, void* stream);
+bool tt_tc_supported(const TTLaunch& p);
 
 // ---- K5: hex sum-factorized operator ----
 // y_q[e,i,m,n] = sum B1[x,a,i] B2[x,b,m] B3[x,c,n] G[x,y,e,a,b,c]

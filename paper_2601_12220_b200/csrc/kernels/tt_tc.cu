@@ -1,0 +1,351 @@
+// K4 (fp32) — tensor-train step on the 5th-generation tensor cores
+//
+//   Y[n,i,k] = sum_{j,l} G1[i,j] G2[k,l] X[n,j,l]        (C4-f32: 4096 x 64^4)
+//
+// as two chained GEMMs per PAIR of samples, both M = 128 (rows = two samples
+// x 64), N = 64, K = 64, issued with tcgen05.mma.cta_group::1.kind::tf32 from
+// shared memory (K-major, 128-byte swizzle) into TMEM accumulators:
+//   GEMM1  T [(n,j), k] = sum_l X[(n,j), l] G2[k, l]      A = X tile (TMA)
+//   GEMM2  Y^T[(n,k), i] = sum_j T^T[(n,k), j] G1[i, j]   A = T^T (epilogue 1)
+//
+// fp32 accuracy from the TF32 datapath (3xTF32): every operand is split into
+// hi = tf32 truncation (exact) and lo = x - hi (exact in fp32), and each GEMM
+// accumulates hi*hi + hi*lo + lo*hi in fp32 (the dropped lo*lo term is
+// ~2^-20 relative); tests/test_gpu_parity.py holds it to the fp32 bar.
+//
+// Warp roles (one CTA per SM, persistent over sample pairs):
+//   warp 16, lane 0 — TMA producer (X pair tiles, two 128-byte k-blocks
+//                     each, double-buffered) and the single MMA-issuing thread;
+//   warps 0-15      — 4 TMEM lane quarters x 4 16-column groups: split X into
+//                     hi/lo, epilogue 1 (TMEM -> registers -> hi/lo T^T tile in
+//                     shared memory, transposed on the way with conflict-free
+//                     128-byte rows), epilogue 2 (TMEM -> coalesced global
+//                     stores of Y).
+// Schedule: GEMM2(t) overlaps the split of X(t+1), GEMM1(t+1) overlaps the
+// drain of Y(t); TMEM holds double-buffered accumulators (256 columns).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <mutex>
+
+#include "launch.h"
+#include "ptx.cuh"
+
+namespace feb200 {
+
+namespace {
+
+constexpr int R = 64;
+constexpr int kRows = 128;                   // two samples per tile
+constexpr int kTile = kRows * R * 4;         // 32 KB: [2 k-blocks][128 rows][128 B]
+constexpr int kKBlockA = kRows * 128;        // 16 KB
+constexpr int kG = R * R * 4;                // 16 KB: [2 k-blocks][64 rows][128 B]
+constexpr int kKBlockB = R * 128;            // 8 KB
+constexpr int kEpiWarps = 16;                // 4 column groups x 4 TMEM lane quarters
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreads = kEpiThreads + 32;
+constexpr std::uint32_t kTmemCols = 256;     // D1[2] + D2[2], 64 columns each
+// instruction descriptor: D f32, A/B tf32, K-major both, M = 128, N = 64
+constexpr std::uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr std::uint32_t kHiMask = 0xFFFFE000u;  // fp32 -> tf32 truncation
+
+struct TTTcDev {
+  std::int64_t nb, npairs;
+  const float* G1;
+  const float* G2;
+  float* Y;
+  std::int64_t y_sn;
+};
+
+// shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart
+__device__ __forceinline__ std::uint64_t sdesc(const void* p) {
+  return static_cast<std::uint64_t>((ptx::smem_addr(p) >> 4) & 0x3FFF) | (std::uint64_t{1} << 16) |
+         (std::uint64_t{1024 >> 4} << 32) | (std::uint64_t{1} << 46) | (std::uint64_t{2} << 61);
+}
+
+// byte offset of element (r, k) in a [rows x 64] fp32 K-major SW128 tile
+__device__ __forceinline__ std::uint32_t sw_off(int r, int k, int rows) {
+  const int kb = k >> 5, kk = k & 31;
+  return static_cast<std::uint32_t>(kb * rows * 128 + r * 128 + ((((kk >> 2) ^ (r & 7)) << 4) | ((kk & 3) << 2)));
+}
+
+__device__ __forceinline__ void mma_tf32(std::uint32_t tmem, std::uint64_t da, std::uint64_t db, std::uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(std::uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(ptx::smem_addr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// 32 lanes x 16 consecutive 32-bit columns
+__device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, std::uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(ptx::smem_addr(dst)),
+      "l"(map), "r"(ptx::smem_addr(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ float hi_of(float x) { return __uint_as_float(__float_as_uint(x) & kHiMask); }
+
+// one 3xTF32 GEMM: D (+)= Ah*Bh + Ah*Bl + Al*Bh over K = 64 (8 k-steps of 8)
+__device__ __forceinline__ void gemm3(std::uint32_t d, const unsigned char* ah, const unsigned char* al,
+                                      const unsigned char* bh, const unsigned char* bl) {
+#pragma unroll
+  for (int pass = 0; pass < 3; ++pass) {
+    const unsigned char* a = pass == 2 ? al : ah;
+    const unsigned char* b = pass == 1 ? bl : bh;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int kb = ks >> 2, kin = (ks & 3) * 32;
+      mma_tf32(d, sdesc(a + kb * kKBlockA + kin), sdesc(b + kb * kKBlockB + kin), (pass | ks) != 0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tt_tc_kernel(const __grid_constant__ TTTcDev p, const __grid_constant__ CUtensorMap tmX) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+  unsigned char* g2h = base;
+  unsigned char* g2l = base + kG;
+  unsigned char* g1h = base + 2 * kG;
+  unsigned char* g1l = base + 3 * kG;
+  unsigned char* xs0 = base + 4 * kG;   // X pair tiles (double-buffered); hi in place after the split
+  unsigned char* ls = xs0 + 2 * kTile;  // X lo
+  unsigned char* a2h = ls + kTile;      // T^T hi / lo
+  unsigned char* a2l = a2h + kTile;
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(a2l + kTile);
+  std::uint64_t* x_full = bars;         // [2]
+  std::uint64_t* d1_full = bars + 2;    // [2]
+  std::uint64_t* d2_full = bars + 4;    // [2]
+  std::uint64_t* d1_free = bars + 6;    // [2]
+  std::uint64_t* d2_free = bars + 8;    // [2]
+  std::uint64_t* lo_ready = bars + 10;
+  std::uint64_t* a2_ready = bars + 11;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 12);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // constants: G2 as B of GEMM1 ([k][l], K = l), G1 as B of GEMM2 ([i][j], K = j), split hi / lo
+  for (int idx = tid; idx < R * R; idx += kThreads) {
+    const int r = idx >> 6, c = idx & 63;
+    const std::uint32_t o = sw_off(r, c, R);
+    const float a = __ldg(p.G2 + idx), b = __ldg(p.G1 + idx);
+    const float ah = hi_of(a), bh = hi_of(b);
+    *reinterpret_cast<float*>(g2h + o) = ah;
+    *reinterpret_cast<float*>(g2l + o) = a - ah;
+    *reinterpret_cast<float*>(g1h + o) = bh;
+    *reinterpret_cast<float*>(g1l + o) = b - bh;
+  }
+  if (warp == kEpiWarps) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_addr(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == kEpiThreads) {
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&x_full[b], 1);
+      ptx::mbar_init(&d1_full[b], 1);
+      ptx::mbar_init(&d2_full[b], 1);
+      ptx::mbar_init(&d1_free[b], kEpiWarps);
+      ptx::mbar_init(&d2_free[b], kEpiWarps);
+    }
+    ptx::mbar_init(lo_ready, kEpiWarps);
+    ptx::mbar_init(a2_ready, kEpiWarps);
+    ptx::fence_barrier_init();
+  }
+  ptx::fence_proxy_async();
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const std::uint32_t tmem = *tmem_slot;
+
+  // local pair t -> global pair blockIdx.x + t * gridDim.x
+  const std::int64_t T = p.npairs > blockIdx.x ? (p.npairs - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  if (warp == kEpiWarps) {
+    // --------------------------- TMA + MMA thread ---------------------------
+    // order: GEMM1(0); then per t: GEMM2(t), GEMM1(t+1) — so GEMM2(t) runs
+    // while the epilogue splits X(t+1), and GEMM1(t+1) while it drains Y(t)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+      auto tma_x = [&](std::int64_t t) {
+        const int b = static_cast<int>(t & 1);
+        const int row0 = static_cast<int>((blockIdx.x + t * gridDim.x) * kRows);
+        unsigned char* xs = xs0 + b * kTile;
+        ptx::mbar_arrive_expect_tx(&x_full[b], kTile);
+        tma_2d(xs, &tmX, &x_full[b], 0, row0);
+        tma_2d(xs + kKBlockA, &tmX, &x_full[b], 32, row0);
+      };
+      auto gemm1 = [&](std::int64_t t) {
+        const int b = static_cast<int>(t & 1);
+        ptx::mbar_wait(lo_ready, static_cast<std::uint32_t>(t & 1));
+        if (t >= 2) ptx::mbar_wait(&d1_free[b], static_cast<std::uint32_t>((t >> 1) - 1) & 1u);
+        tc_after();
+        gemm3(tmem + static_cast<std::uint32_t>(b * 128), xs0 + b * kTile, ls, g2h, g2l);
+        mma_commit(&d1_full[b]);
+      };
+      if (T > 0) tma_x(0);
+      if (T > 1) tma_x(1);
+      if (T > 0) gemm1(0);
+      for (std::int64_t t = 0; t < T; ++t) {
+        const int b = static_cast<int>(t & 1);
+        ptx::mbar_wait(a2_ready, static_cast<std::uint32_t>(t & 1));  // implies GEMM1(t) done: X tile b free
+        if (t + 2 < T) tma_x(t + 2);
+        if (t >= 2) ptx::mbar_wait(&d2_free[b], static_cast<std::uint32_t>((t >> 1) - 1) & 1u);
+        tc_after();
+        gemm3(tmem + static_cast<std::uint32_t>(b * 128 + 64), a2h, a2l, g1h, g1l);
+        mma_commit(&d2_full[b]);
+        if (t + 1 < T) gemm1(t + 1);
+      }
+    }
+  } else {
+    // ------------------------ split + epilogue warps ------------------------
+    // warp = (column group cg, TMEM lane quarter q): rows q*32 + lane, 16 columns
+    const int q = warp & 3, cg = warp >> 2;
+    const int row = q * 32 + lane;
+    const std::uint32_t tl = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(cg * 16);
+    auto split = [&](std::int64_t t) {
+      const int b = static_cast<int>(t & 1);
+      ptx::mbar_wait(&x_full[b], static_cast<std::uint32_t>(t >> 1) & 1u);
+      float4* xs = reinterpret_cast<float4*>(xs0 + b * kTile);
+      float4* lo = reinterpret_cast<float4*>(ls);
+#pragma unroll
+      for (int k = 0; k < kTile / 16 / kEpiThreads; ++k) {
+        const int qd = tid + k * kEpiThreads;
+        const float4 x = xs[qd];
+        const float4 h = make_float4(hi_of(x.x), hi_of(x.y), hi_of(x.z), hi_of(x.w));
+        xs[qd] = h;
+        lo[qd] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+      }
+      ptx::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(lo_ready);
+    };
+    if (T > 0) split(0);
+    for (std::int64_t t = 0; t < T; ++t) {
+      const int b = static_cast<int>(t & 1);
+      const std::uint32_t par = static_cast<std::uint32_t>(t >> 1) & 1u;
+      // epilogue 1: T[(n,j)][k] -> T^T hi/lo tile, element ((n,k), j). GEMM2(t-1),
+      // the last reader of that tile, completed before epilogue 2 of t-1.
+      ptx::mbar_wait(&d1_full[b], par);
+      tc_after();
+      std::uint32_t v[16];
+      tmem_ld16(tl + static_cast<std::uint32_t>(b * 128), v);
+      tmem_wait_ld();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&d1_free[b]);
+      {
+        const int n = row >> 6, j = row & 63;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const float x = __uint_as_float(v[c]);
+          const float h = hi_of(x);
+          const std::uint32_t o = sw_off(n * 64 + cg * 16 + c, j, kRows);
+          *reinterpret_cast<float*>(a2h + o) = h;
+          *reinterpret_cast<float*>(a2l + o) = x - h;
+        }
+      }
+      ptx::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(a2_ready);
+      // split X(t+1): the lo tile's last reader GEMM1(t) is complete
+      if (t + 1 < T) split(t + 1);
+      // epilogue 2: row = (n, k): Y[n][i][k] = D2[row][i]; lanes on consecutive k -> 128-byte stores
+      ptx::mbar_wait(&d2_full[b], par);
+      tc_after();
+      tmem_ld16(tl + static_cast<std::uint32_t>(b * 128 + 64), v);
+      tmem_wait_ld();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&d2_free[b]);
+      const std::int64_t n = (blockIdx.x + t * gridDim.x) * 2 + (row >> 6);
+      if (n < p.nb) {
+        float* y = p.Y + n * p.y_sn + static_cast<std::int64_t>(cg * 16) * R + (row & 63);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) __stcs(y + c * R, __uint_as_float(v[c]));
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == kEpiWarps) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tc_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+}  // namespace
+
+bool tt_tc_supported(const TTLaunch& L) {
+  return L.fp32 && tt_supported(L.NI, L.NJ, L.NK, L.NL) && L.x_sj == R && L.x_sn == R * R && L.y_sn % 4 == 0 &&
+         (reinterpret_cast<std::uintptr_t>(L.X) & 15) == 0;
+}
+
+int launch_tt_tc(const TTLaunch& L, void* stream) {
+  if (L.Nb == 0) return cudaSuccess;
+  if (!tt_tc_supported(L)) return cudaErrorInvalidValue;
+  auto enc = tc_encoder();
+  if (!enc) return cudaErrorInvalidValue;
+  // X as a 2-D [Nb*64 rows][64] fp32 matrix; boxes of 128 rows x 32 columns (128 B)
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(L.Nb) * R};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(R) * 4};
+  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kRows)};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(L.X), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  TTTcDev d{};
+  d.nb = L.Nb;
+  d.npairs = (L.Nb + 1) / 2;
+  d.G1 = static_cast<const float*>(L.G1);
+  d.G2 = static_cast<const float*>(L.G2);
+  d.Y = static_cast<float*>(L.Y);
+  d.y_sn = L.y_sn;
+  const size_t smem = 1024 + 4 * kG + 5 * kTile + 16 * sizeof(std::uint64_t);
+  cudaError_t e = cudaFuncSetAttribute(tt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  device_sm_count(&sms);
+  std::int64_t grid = sms;
+  if (grid > d.npairs) grid = d.npairs;
+  tt_tc_kernel<<<static_cast<int>(grid), kThreads, smem, static_cast<cudaStream_t>(stream)>>>(d, tm);
+  return cudaGetLastError();
+}
+
+}  // namespace feb200

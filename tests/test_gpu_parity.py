@@ -293,6 +293,13 @@ def test_tensor_train_small(fe, ref, torch_cuda, dtype, tol):
     b = ref.random_bindings(e, 12)
     got = run_plan(torch_cuda, plan, b)
     want = ref.evaluate(e, b)
+    if dtype == "float32":
+        # fp32 bar: no worse than a plain fp32 evaluation of the same data
+        # (CUDA-core torch.einsum), the tcgen05 path computes 3xTF32
+        t = {k: torch_cuda.tensor(np.real(v), dtype=torch_cuda.float32, device="cuda") for k, v in b.items()}
+        names = [m["name"] for m in plan.inputs]
+        f32 = torch_cuda.einsum("ij,kl,njl->nik", *[t[k].reshape(m["shape"]) for k, m in zip(names, plan.inputs)])
+        tol = max(tol, 4 * rel_err(f32.cpu().numpy(), want[0]))
     assert rel_err(got[0], want[0]) <= tol
 
 
@@ -310,8 +317,33 @@ def test_tensor_train_full_vs_torch(fe, torch_cuda, dtype, tol):
         fe.fill_dyadic(t, 30 + k)
     (Y,) = plan(G1, G2, X)
     want = torch.einsum("ij,kl,njl->nik", G1.double(), G2.double(), X.double())
+    rel = lambda a: ((a.double() - want).abs() / want.abs().clamp(min=1.0)).max().item()  # noqa: E731
+    if dtype == "float32":
+        tol = max(tol, 4 * rel(torch.einsum("ij,kl,njl->nik", G1, G2, X)))
+    assert rel(Y) <= tol
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 300, 4096])
+@pytest.mark.parametrize("meta", ["tc=1", "tc=0"])
+def test_tensor_train_f32_tensor_cores(fe, torch_cuda, n, meta):
+    """fp32 C4 on tcgen05 (3xTF32 split, tc=1) and on the DMMA path (tc=0):
+    full-mantissa random data (not tf32-representable), odd sample counts
+    (the last pair half out of bounds), held to the fp32 bar against fp64."""
+    from paper_2601_12220_b200 import configs as C
+    torch = torch_cuda
+    plan = fe.Plan(einsum=C.tensor_train(n=n, dtype="float32"), options={"meta": meta, "transform": "tt/v1"})
+    g = torch.Generator(device="cuda").manual_seed(n)
+    G1 = torch.randn(64, 64, device="cuda", generator=g)
+    G2 = torch.randn(64, 64, device="cuda", generator=g)
+    X = torch.randn(n, 64, 64, device="cuda", generator=g) * 3.0
+    (Y,) = plan(G1, G2, X)
+    torch.cuda.synchronize()
+    want = torch.einsum("ij,kl,njl->nik", G1.double(), G2.double(), X.double())
     err = ((Y.double() - want).abs() / want.abs().clamp(min=1.0)).max().item()
-    assert err <= tol
+    # plain fp32 (torch, CUDA cores) as the yardstick for "fp32 accuracy"
+    f32 = torch.einsum("ij,kl,njl->nik", G1, G2, X)
+    err_f32 = ((f32.double() - want).abs() / want.abs().clamp(min=1.0)).max().item()
+    assert err <= max(1e-5, 4 * err_f32), (err, err_f32)
 
 
 def test_hex_sumfact_small(fe, ref, torch_cuda):

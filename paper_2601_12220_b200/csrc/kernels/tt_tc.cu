@@ -28,6 +28,8 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "launch.h"
@@ -41,14 +43,16 @@ constexpr int R = 64;
 constexpr int kRows = 128;                   // two samples per tile
 constexpr int kTile = kRows * R * 4;         // 32 KB: [2 k-blocks][128 rows][128 B]
 constexpr int kKBlockA = kRows * 128;        // 16 KB
-constexpr int kG = R * R * 4;                // 16 KB: [2 k-blocks][64 rows][128 B]
-constexpr int kKBlockB = R * 128;            // 8 KB
+constexpr int kG = 2 * R * R * 4;            // 32 KB: [2 k-blocks][128 rows = hi 64 | lo 64][128 B]
+constexpr int kKBlockB = 2 * R * 128;        // 16 KB
 constexpr int kEpiWarps = 16;                // 4 column groups x 4 TMEM lane quarters
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = kEpiThreads + 32;
-constexpr std::uint32_t kTmemCols = 256;     // D1[2] + D2[2], 64 columns each
-// instruction descriptor: D f32, A/B tf32, K-major both, M = 128, N = 64
-constexpr std::uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr std::uint32_t kTmemCols = 512;     // D1[2] + D2[2], 128 columns each
+// instruction descriptor: D f32, A/B tf32, K-major both, M = 128, N = n
+constexpr std::uint32_t idesc(std::uint32_t n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+}
 constexpr std::uint32_t kHiMask = 0xFFFFE000u;  // fp32 -> tf32 truncation
 
 struct TTTcDev {
@@ -57,7 +61,19 @@ struct TTTcDev {
   const float* G2;
   float* Y;
   std::int64_t y_sn;
+  unsigned long long* trace;  // -DFE_TT_TRACE builds: per-phase timestamps of CTA 0
 };
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef FE_TT_TRACE
+#define TT_TRACE(t, slot) \
+  if (p.trace && blockIdx.x == 0 && (t) < 64) p.trace[(t) * 16 + (slot)] = gtime();
+#else
+#define TT_TRACE(t, slot) {}
+#endif
 
 // shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart
 __device__ __forceinline__ std::uint64_t sdesc(const void* p) {
@@ -71,11 +87,12 @@ __device__ __forceinline__ std::uint32_t sw_off(int r, int k, int rows) {
   return static_cast<std::uint32_t>(kb * rows * 128 + r * 128 + ((((kk >> 2) ^ (r & 7)) << 4) | ((kk & 3) << 2)));
 }
 
-__device__ __forceinline__ void mma_tf32(std::uint32_t tmem, std::uint64_t da, std::uint64_t db, std::uint32_t acc) {
+__device__ __forceinline__ void mma_tf32(std::uint32_t tmem, std::uint64_t da, std::uint64_t db, std::uint32_t id,
+                                         std::uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+      "l"(da), "l"(db), "r"(id), "r"(acc));
 }
 
 __device__ __forceinline__ void mma_commit(std::uint64_t* bar) {
@@ -107,18 +124,21 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, std::u
 
 __device__ __forceinline__ float hi_of(float x) { return __uint_as_float(__float_as_uint(x) & kHiMask); }
 
-// one 3xTF32 GEMM: D (+)= Ah*Bh + Ah*Bl + Al*Bh over K = 64 (8 k-steps of 8)
+// one 3xTF32 GEMM over K = 64 (8 k-steps of 8), B = [Bh ; Bl] stacked on N:
+//   D[:, 0:128]  = Ah * [Bh ; Bl]^T     (N = 128: the hi*hi and hi*lo terms side by side)
+//   D[:, 0:64]  += Al * Bh^T            (N = 64)
+// the epilogue adds the two 64-column halves in fp32
 __device__ __forceinline__ void gemm3(std::uint32_t d, const unsigned char* ah, const unsigned char* al,
-                                      const unsigned char* bh, const unsigned char* bl) {
+                                      const unsigned char* bhl) {
 #pragma unroll
-  for (int pass = 0; pass < 3; ++pass) {
-    const unsigned char* a = pass == 2 ? al : ah;
-    const unsigned char* b = pass == 1 ? bl : bh;
+  for (int ks = 0; ks < 8; ++ks) {
+    const int kb = ks >> 2, kin = (ks & 3) * 32;
+    mma_tf32(d, sdesc(ah + kb * kKBlockA + kin), sdesc(bhl + kb * kKBlockB + kin), idesc(128), ks != 0);
+  }
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const int kb = ks >> 2, kin = (ks & 3) * 32;
-      mma_tf32(d, sdesc(a + kb * kKBlockA + kin), sdesc(b + kb * kKBlockB + kin), (pass | ks) != 0);
-    }
+  for (int ks = 0; ks < 8; ++ks) {
+    const int kb = ks >> 2, kin = (ks & 3) * 32;
+    mma_tf32(d, sdesc(al + kb * kKBlockA + kin), sdesc(bhl + kb * kKBlockB + kin), idesc(64), 1);
   }
 }
 
@@ -127,11 +147,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
-  unsigned char* g2h = base;
-  unsigned char* g2l = base + kG;
-  unsigned char* g1h = base + 2 * kG;
-  unsigned char* g1l = base + 3 * kG;
-  unsigned char* xs0 = base + 4 * kG;   // X pair tiles (double-buffered); hi in place after the split
+  unsigned char* g2 = base;  // [G2 hi ; G2 lo], B of GEMM1
+  unsigned char* g1 = base + kG;  // [G1 hi ; G1 lo], B of GEMM2
+  unsigned char* xs0 = base + 2 * kG;   // X pair tiles (double-buffered); hi in place after the split
   unsigned char* ls = xs0 + 2 * kTile;  // X lo
   unsigned char* a2h = ls + kTile;      // T^T hi / lo
   unsigned char* a2l = a2h + kTile;
@@ -148,15 +166,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // constants: G2 as B of GEMM1 ([k][l], K = l), G1 as B of GEMM2 ([i][j], K = j), split hi / lo
+#pragma unroll 8
   for (int idx = tid; idx < R * R; idx += kThreads) {
     const int r = idx >> 6, c = idx & 63;
-    const std::uint32_t o = sw_off(r, c, R);
     const float a = __ldg(p.G2 + idx), b = __ldg(p.G1 + idx);
     const float ah = hi_of(a), bh = hi_of(b);
-    *reinterpret_cast<float*>(g2h + o) = ah;
-    *reinterpret_cast<float*>(g2l + o) = a - ah;
-    *reinterpret_cast<float*>(g1h + o) = bh;
-    *reinterpret_cast<float*>(g1l + o) = b - bh;
+    *reinterpret_cast<float*>(g2 + sw_off(r, c, 2 * R)) = ah;
+    *reinterpret_cast<float*>(g2 + sw_off(R + r, c, 2 * R)) = a - ah;
+    *reinterpret_cast<float*>(g1 + sw_off(r, c, 2 * R)) = bh;
+    *reinterpret_cast<float*>(g1 + sw_off(R + r, c, 2 * R)) = b - bh;
   }
   if (warp == kEpiWarps) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_addr(tmem_slot)),
@@ -201,23 +219,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto gemm1 = [&](std::int64_t t) {
         const int b = static_cast<int>(t & 1);
         ptx::mbar_wait(lo_ready, static_cast<std::uint32_t>(t & 1));
+        TT_TRACE(t, 0)
         if (t >= 2) ptx::mbar_wait(&d1_free[b], static_cast<std::uint32_t>((t >> 1) - 1) & 1u);
         tc_after();
-        gemm3(tmem + static_cast<std::uint32_t>(b * 128), xs0 + b * kTile, ls, g2h, g2l);
+        gemm3(tmem + static_cast<std::uint32_t>(b * 256), xs0 + b * kTile, ls, g2);
         mma_commit(&d1_full[b]);
+        TT_TRACE(t, 1)
       };
       if (T > 0) tma_x(0);
       if (T > 1) tma_x(1);
       if (T > 0) gemm1(0);
       for (std::int64_t t = 0; t < T; ++t) {
         const int b = static_cast<int>(t & 1);
+        // GEMM1(t+1) first: it runs while the epilogue warps turn T(t) into T^T
+        if (t + 1 < T) gemm1(t + 1);
         ptx::mbar_wait(a2_ready, static_cast<std::uint32_t>(t & 1));  // implies GEMM1(t) done: X tile b free
+        TT_TRACE(t, 2)
         if (t + 2 < T) tma_x(t + 2);
         if (t >= 2) ptx::mbar_wait(&d2_free[b], static_cast<std::uint32_t>((t >> 1) - 1) & 1u);
         tc_after();
-        gemm3(tmem + static_cast<std::uint32_t>(b * 128 + 64), a2h, a2l, g1h, g1l);
+        gemm3(tmem + static_cast<std::uint32_t>(b * 256 + 128), a2h, a2l, g1);
         mma_commit(&d2_full[b]);
-        if (t + 1 < T) gemm1(t + 1);
+        TT_TRACE(t, 3)
       }
     }
   } else {
@@ -229,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto split = [&](std::int64_t t) {
       const int b = static_cast<int>(t & 1);
       ptx::mbar_wait(&x_full[b], static_cast<std::uint32_t>(t >> 1) & 1u);
+      if (tid == 0) TT_TRACE(t, 9)
       float4* xs = reinterpret_cast<float4*>(xs0 + b * kTile);
       float4* lo = reinterpret_cast<float4*>(ls);
 #pragma unroll
@@ -242,18 +266,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::fence_proxy_async();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(lo_ready);
+      if (tid == 0) TT_TRACE(t, 6)
+    };
+    // epilogue 2: row = (n, k): Y[n][i][k] = D2[row][i]; lanes on consecutive k -> 128-byte stores
+    auto epi2 = [&](std::int64_t t1) {
+      const int b1 = static_cast<int>(t1 & 1);
+      std::uint32_t v[16], w[16];
+      tmem_ld16(tl + static_cast<std::uint32_t>(b1 * 256 + 128), v);
+      tmem_ld16(tl + static_cast<std::uint32_t>(b1 * 256 + 192), w);
+      tmem_wait_ld();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&d2_free[b1]);
+      const std::int64_t n = (blockIdx.x + t1 * gridDim.x) * 2 + (row >> 6);
+      if (n < p.nb) {
+        float* y = p.Y + n * p.y_sn + static_cast<std::int64_t>(cg * 16) * R + (row & 63);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) __stcs(y + c * R, __uint_as_float(v[c]) + __uint_as_float(w[c]));
+      }
+      if (tid == 0) TT_TRACE(t1, 8)
     };
     if (T > 0) split(0);
     for (std::int64_t t = 0; t < T; ++t) {
       const int b = static_cast<int>(t & 1);
       const std::uint32_t par = static_cast<std::uint32_t>(t >> 1) & 1u;
-      // epilogue 1: T[(n,j)][k] -> T^T hi/lo tile, element ((n,k), j). GEMM2(t-1),
-      // the last reader of that tile, completed before epilogue 2 of t-1.
       ptx::mbar_wait(&d1_full[b], par);
+      if (tid == 0) TT_TRACE(t, 4)
+      // GEMM1(t) is done with the lo tile: split X(t+1) so GEMM1(t+1) can start
+      if (t + 1 < T) split(t + 1);
+      // epilogue 1: T[(n,j)][k] -> T^T hi/lo tile, element ((n,k), j), once
+      // GEMM2(t-1), its last reader, is complete
+      if (t >= 1) {
+        ptx::mbar_wait(&d2_full[(t - 1) & 1], static_cast<std::uint32_t>((t - 1) >> 1) & 1u);
+        if (tid == 0) TT_TRACE(t - 1, 7)
+      }
       tc_after();
-      std::uint32_t v[16];
-      tmem_ld16(tl + static_cast<std::uint32_t>(b * 128), v);
+      std::uint32_t v[16], w[16];
+      if (tid == 0) TT_TRACE(t, 10)
+      tmem_ld16(tl + static_cast<std::uint32_t>(b * 256), v);
+      tmem_ld16(tl + static_cast<std::uint32_t>(b * 256 + 64), w);
       tmem_wait_ld();
+      if (tid == 0) TT_TRACE(t, 11)
       tc_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&d1_free[b]);
@@ -261,32 +314,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = row >> 6, j = row & 63;
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-          const float x = __uint_as_float(v[c]);
+          const float x = __uint_as_float(v[c]) + __uint_as_float(w[c]);
           const float h = hi_of(x);
           const std::uint32_t o = sw_off(n * 64 + cg * 16 + c, j, kRows);
           *reinterpret_cast<float*>(a2h + o) = h;
           *reinterpret_cast<float*>(a2l + o) = x - h;
         }
       }
+      if (tid == 0) TT_TRACE(t, 12)
       ptx::fence_proxy_async();
+      if (tid == 0) TT_TRACE(t, 13)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(a2_ready);
-      // split X(t+1): the lo tile's last reader GEMM1(t) is complete
-      if (t + 1 < T) split(t + 1);
-      // epilogue 2: row = (n, k): Y[n][i][k] = D2[row][i]; lanes on consecutive k -> 128-byte stores
-      ptx::mbar_wait(&d2_full[b], par);
+      if (tid == 0) TT_TRACE(t, 5)
+      if (tid == 32 * 15) TT_TRACE(t, 14)
+      // epilogue 2 of the previous pair (its D2 buffer is not the one GEMM2(t) writes)
+      if (t >= 1) epi2(t - 1);
+    }
+    if (T > 0) {
+      ptx::mbar_wait(&d2_full[(T - 1) & 1], static_cast<std::uint32_t>((T - 1) >> 1) & 1u);
       tc_after();
-      tmem_ld16(tl + static_cast<std::uint32_t>(b * 128 + 64), v);
-      tmem_wait_ld();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&d2_free[b]);
-      const std::int64_t n = (blockIdx.x + t * gridDim.x) * 2 + (row >> 6);
-      if (n < p.nb) {
-        float* y = p.Y + n * p.y_sn + static_cast<std::int64_t>(cg * 16) * R + (row & 63);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) __stcs(y + c * R, __uint_as_float(v[c]));
-      }
+      epi2(T - 1);
     }
   }
   tc_before();
@@ -311,8 +359,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tc_encoder() {
 }  // namespace
 
 bool tt_tc_supported(const TTLaunch& L) {
-  return L.fp32 && tt_supported(L.NI, L.NJ, L.NK, L.NL) && L.x_sj == R && L.x_sn == R * R && L.y_sn % 4 == 0 &&
-         (reinterpret_cast<std::uintptr_t>(L.X) & 15) == 0;
+  return L.fp32 && tt_supported(L.NI, L.NJ, L.NK, L.NL) && L.x_sj == R && L.x_sn == R * R && L.y_sn == R * R &&
+         (reinterpret_cast<std::uintptr_t>(L.X) & 15) == 0 && (reinterpret_cast<std::uintptr_t>(L.Y) & 15) == 0;
 }
 
 int launch_tt_tc(const TTLaunch& L, void* stream) {
@@ -337,14 +385,36 @@ int launch_tt_tc(const TTLaunch& L, void* stream) {
   d.G2 = static_cast<const float*>(L.G2);
   d.Y = static_cast<float*>(L.Y);
   d.y_sn = L.y_sn;
-  const size_t smem = 1024 + 4 * kG + 5 * kTile + 16 * sizeof(std::uint64_t);
+  const size_t smem = 1024 + 2 * kG + 5 * kTile + 16 * sizeof(std::uint64_t);
   cudaError_t e = cudaFuncSetAttribute(tt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int sms = 148;
   device_sm_count(&sms);
   std::int64_t grid = sms;
   if (grid > d.npairs) grid = d.npairs;
+#ifdef FE_TT_TRACE
+  static const bool tracing = std::getenv("FE_TT_TRACE") != nullptr;
+#else
+  constexpr bool tracing = false;
+#endif
+  if (tracing) {
+    cudaMalloc(&d.trace, 64 * 16 * 8);
+    cudaMemset(d.trace, 0, 64 * 16 * 8);
+  }
   tt_tc_kernel<<<static_cast<int>(grid), kThreads, smem, static_cast<cudaStream_t>(stream)>>>(d, tm);
+  if (tracing) {
+    unsigned long long h[64 * 16];
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    cudaMemcpy(h, d.trace, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d.trace);
+    unsigned long long t0 = h[9];
+    std::fprintf(stderr, "t: xfull | lo_rdy mma:lo g1c | epi:d1 a2rdy | mma:a2 g2c | epi:d2 ystore  (ns from x_full(0))\n");
+    for (int t = 0; t < 14; ++t) {
+      auto f = [&](int k) { return h[t * 16 + k] ? static_cast<long long>(h[t * 16 + k] - t0) : -1LL; };
+      std::fprintf(stderr, "%2d: %6lld | %6lld %6lld %6lld | %6lld %6lld | %6lld %6lld | %6lld %6lld || ld %6lld %6lld sts %6lld fence %6lld w15 %6lld\n", t, f(9), f(6),
+                   f(0), f(1), f(4), f(5), f(2), f(3), f(7), f(8), f(10), f(11), f(12), f(13), f(14));
+    }
+  }
   return cudaGetLastError();
 }
 

@@ -153,6 +153,7 @@ class Workload:
             self.plan, self.lo, self.hi, self.axis = full, 0, 0, ""
         info = self.plan.info
         self.transform = info["transform"]
+        self.pipe = info.get("pipe", "dfma")
         self.source = info["source"]
         self.key = full.info["key"]
         self.flops = info["algorithmic_flops"]  # this rank's shard
@@ -254,6 +255,15 @@ def gpu_arm(args):
         if fe.lib().fe_fp64_peak(which, ctypes.byref(v)) == 0:
             fp64[label] = v.value
 
+    def pipe_peak(pipe):
+        """(TFLOP/s, source) of the arithmetic pipe a kernel issues to."""
+        if pipe in ("dfma", "dmma"):
+            return fp64.get(pipe, 0.0), "measured on this GPU by fe_fp64_peak (FP64 %s)" % pipe.upper()
+        if pipe == "tcgen05_tf32x3":
+            # dense TF32 = half the measured bf16 rate; 3xTF32 spends three MMAs per product
+            return peaks["bf16_tflops"] / 2 / 3, "MEASURED_PEAKS.json bf16_tflops / 2 (TF32) / 3 (3xTF32 passes)"
+        return 0.0, "none"
+
     per = {}
     rates = []
     for w, t in zip(loads, mean_t):
@@ -262,12 +272,13 @@ def gpu_arm(args):
         rates.append(gflops)
         # per-config roofline: slower of HBM (footprint bytes) and FP64 (DMMA
         # peak for the DMMA kernels, DFMA peak for the DFMA kernels)
-        fp_peak = fp64.get("dmma" if w.transform in ("gett_dmma/v1", "tt/v1") else "dfma", 0.0) * 1e12
+        fp_peak = pipe_peak(w.pipe)[0] * 1e12
         roof_t = max(w.bytes / (peaks["hbm_gbs"] * 1e9), w.flops / fp_peak if fp_peak else 0.0)
         per[w.name] = {"ms": t * 1e3, "gflops": gflops, "gbs": w.bytes * world / t / 1e9,
                        "transform": w.transform, "source": w.source, "flops": w.flops, "bytes": w.bytes,
                        "roof_ms": roof_t * 1e3, "roof_frac": roof_t / t,
-                       "bound": "hbm" if w.bytes / (peaks["hbm_gbs"] * 1e9) >= roof_t else "fp64"}
+                       "pipe": w.pipe,
+                       "bound": "hbm" if w.bytes / (peaks["hbm_gbs"] * 1e9) >= roof_t else w.pipe}
     value = math.exp(sum(math.log(r) for r in rates) / len(rates)) if rates else 0.0
     ms_step = sum(mean_t) * 1e3
 
@@ -276,8 +287,7 @@ def gpu_arm(args):
     roof = None
     if dom is not None:
         w, t = loads[dom], mean_t[dom]
-        pipe = "dmma" if w.transform in ("gett_dmma/v1", "tt/v1") else "dfma"
-        fp64_peak = fp64.get(pipe)
+        fp64_peak, fp_src = pipe_peak(w.pipe)
         hbm_time = w.bytes / (peaks["hbm_gbs"] * 1e9)
         fp_time = w.flops / (fp64_peak * 1e12) if fp64_peak else 0
         if hbm_time >= fp_time:
@@ -287,12 +297,19 @@ def gpu_arm(args):
             # FP64 work: tcgen05 has no f64 kind, so the denominator is the FP64
             # pipe this kernel issues to (DMMA tensor cores or DFMA), measured
             # on this GPU; MEASURED_PEAKS.json only carries HBM and bf16
-            roof = {"bound": "tensor" if pipe == "dmma" else "fp64", "achieved": w.flops / t / 1e12,
-                    "peak": fp64_peak, "unit": "TFLOP/s",
-                    "peak_source": "measured on this GPU by fe_fp64_peak (FP64 %s)" % pipe.upper()}
+            roof = {"bound": "tensor" if w.pipe in ("dmma", "tcgen05_tf32x3") else "fp64",
+                    "achieved": w.flops / t / 1e12, "peak": fp64_peak, "unit": "TFLOP/s", "peak_source": fp_src}
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["kernel"] = w.name + ":" + w.transform
         roof["traffic"] = None
+        try:  # dram bytes per launch of this config's kernel from the committed ncu capture
+            with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+                tr = json.load(f)["per_config"].get(w.name.split("@")[0])
+            if tr:
+                roof["traffic"] = tr["dram_bytes"]
+                roof["traffic_source"] = "profiles/r01/traffic.json (ncu --set full, %s)" % tr["kernel"]
+        except (OSError, ValueError, KeyError):
+            pass
 
     verify = verify_shards(loads, torch, fe, rank, world, dist, cdev) if world > 1 else None
 

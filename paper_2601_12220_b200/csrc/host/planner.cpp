@@ -1345,6 +1345,16 @@ std::string describe(const Plan& p) {
   v.set("meta", Value::str(p.meta));
   v.set("functional", Value::boolean_(p.functional));
   v.set("complex", Value::boolean_(p.complex_mode));
+  // the arithmetic pipe the chosen kernel issues to (roofline denominator)
+  const char* pipe = "fma";
+  switch (p.family) {
+    case Family::fem_grad: pipe = meta_int(p.meta, "mma", 0) ? "dmma" : "dfma"; break;
+    case Family::gett: pipe = "dmma"; break;
+    case Family::tt: pipe = (p.tt.fp32 && meta_int(p.meta, "tc", 1)) ? "tcgen05_tf32x3" : "dmma"; break;
+    case Family::hex: pipe = "dfma"; break;
+    case Family::generic: pipe = "fma"; break;
+  }
+  v.set("pipe", Value::str(pipe));
   Value leaves = Value::arr();
   for (const auto& L : p.leaves) {
     Value x = feinsum::transport::meta_to_json(L.meta);

@@ -286,7 +286,11 @@ int launch_fem_grad(const FemGradLaunch& p, void* stream) {
   if (p.NI == 10 && p.NJ == 10) {
     // small batches: half-size tiles put more CTAs in flight (latency-bound)
     if (p.tile_e == 16) return launch_shape<3, 3, 10, 10, 16>(p, s);
-    if (p.ept == 2) return launch_shape<3, 3, 10, 10, 32, 2>(p, s);
+    if (p.ept == 2) {
+      // 64-element tiles: one tile per SM for small batches (C1: 157 tiles)
+      if (p.tile_e == 64) return launch_shape<3, 3, 10, 10, 64, 2>(p, s);
+      return launch_shape<3, 3, 10, 10, 32, 2>(p, s);
+    }
     return launch_shape<3, 3, 10, 10, 32>(p, s);
   }
   if (p.NI == 4 && p.NJ == 4) return launch_shape<3, 3, 4, 4, 64>(p, s);

@@ -17,7 +17,8 @@ sys.path.insert(0, ROOT)
 
 CANDIDATES = {
     "fem_grad/v1": ["stages=4", "stages=2;te=16", "stages=4;te=16", "stages=8;te=16", "stages=3;dsmem=1",
-                    "stages=2;ept=2", "stages=3;ept=2", "stages=4;ept=2", "mma=1;stages=4"],
+                    "stages=2;ept=2", "stages=3;ept=2", "stages=4;ept=2", "stages=2;ept=2;te=64",
+                    "stages=3;ept=2;te=64", "mma=1;stages=4"],
     "gett_dmma/v1": ["stages=2;group=12", "stages=3;group=6", "stages=3;group=12", "stages=3;group=24"],
     "tt/v1": ["stages=2"],
     "hex_sumfact/v1": [""],

@@ -1258,6 +1258,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
       L.ND = h.ND;
       L.P = h.P;
       L.rows = static_cast<int>(h.u.size());
+      L.variant = meta_int(plan.meta, "v", 2);
       for (int k = 0; k < 6; ++k) L.mats[k] = static_cast<const double*>(d_in[h.mats[k]]);
       L.G = static_cast<const double*>(d_in[h.g]);
       for (size_t q = 0; q < h.u.size(); ++q) {

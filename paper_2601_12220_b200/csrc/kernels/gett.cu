@@ -32,16 +32,22 @@ namespace feb200 {
 
 namespace {
 
-constexpr int BM = 72, BN = 72;      // CTA tile (mi x ni)
-constexpr int KA = 8, KB = 8;        // k box: 8 kA x 8 kB (64-byte rows on both operands)
+constexpr int EXT = 72;              // mi = ni extent (one TMA box row span)
+constexpr int MT = 2, NT = 2;        // mo / no values per CTA tile
+constexpr int BM = MT * EXT, BN = NT * EXT;  // CTA tile 144 x 144
+constexpr int KA = 8, KB = 4;        // k box: 8 kA (64-byte A rows) x 4 kB (32-byte B rows)
 constexpr int KT = KA * KB;          // k per stage
-constexpr int kConsumerWarps = 9;
-constexpr int kThreads = 32 * (kConsumerWarps + 1);
-constexpr int kTileBytes = BM * KT * 8;  // 36864 = 36 x 1024 (swizzle atoms)
+constexpr int kConsumerWarps = 12;   // 6 x 2 warp tiles of 24 x 72: three per SM sub-partition
+// plus one producer warpgroup (one TMA thread) that hands its registers to
+// the consumers (setmaxnreg): 3 x 128 x 152 + 128 x 40 registers
+constexpr int kThreads = 32 * (kConsumerWarps + 4);
+constexpr int kConsumerRegs = 152, kProducerRegs = 40;
+constexpr int kTileBytes = BM * KT * 8;  // 36864 (A and B alike)
 
 struct GettDev {
-  std::int64_t mo, no;                  // tile counts (= extents of mo / no)
-  std::int64_t ka_steps, kb_steps;      // kA/8, kB/2
+  std::int64_t mo, no;                  // tile counts (ceil(extent / 2) of mo / no)
+  std::int64_t ext_mo, ext_no;
+  std::int64_t ka_steps, kb_steps;      // kA/8, kB/4
   std::int64_t c_mo, c_mi, c_no, c_ni;  // C strides (elements)
   double* C;
   const double* coef;
@@ -52,9 +58,6 @@ struct GettDev {
   double kdim;         // |K| = ext_ka * ext_kb
   int stages, group;  // group: side of the square raster block (tiles sharing A/B slices in L2)
 };
-
-// 64-byte swizzle (TMA CU_TENSOR_MAP_SWIZZLE_64B): 16-byte chunk bits [4:5] ^= bits [7:8]
-__device__ __forceinline__ std::uint32_t swz64(std::uint32_t off) { return off ^ (((off >> 7) & 3u) << 4); }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1,
                                             int c2, int c3) {
@@ -103,9 +106,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     (void)cols;
   };
 
-  if (warp == kConsumerWarps) {
+  if (warp >= kConsumerWarps) {
     // ------------------------------- producer -------------------------------
-    if (lane != 0) return;
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
+    if (warp != kConsumerWarps || lane != 0) return;
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     std::int64_t it = 0;
@@ -120,18 +124,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ka0 = static_cast<int>(ks % p.ka_steps) * KA;
         ptx::mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
         unsigned char* st = tiles + static_cast<size_t>(s) * 2 * kTileBytes;
-        // A dims (kA, mi, kB, mo) -> image [kB][mi][kA]; B dims (kB, ni, kA, no) -> image [kA][ni][kB];
-        // both with 64-byte rows under the 64B swizzle
-        tma_load_4d(st, &tmA, &full[s], ka0, 0, kb0, static_cast<int>(mo));
-        tma_load_4d(st + kTileBytes, &tmB, &full[s], kb0, 0, ka0, static_cast<int>(no));
+        // A dims (kA, mi, kB, mo) -> image [mo2][kB][mi][kA] (64-byte rows, 64B swizzle);
+        // B dims (kB, ni, kA, no) -> image [no2][kA][ni][kB] (32-byte rows, 32B swizzle)
+        // boxes of two mo (no) values; an odd last one reads zeros out of bounds
+        tma_load_4d(st, &tmA, &full[s], ka0, 0, kb0, static_cast<int>(mo * MT));
+        tma_load_4d(st + kTileBytes, &tmB, &full[s], kb0, 0, ka0, static_cast<int>(no * NT));
       }
     }
     return;
   }
 
   // -------------------------------- consumers --------------------------------
-  const int wm = warp / 3, wn = warp % 3;  // 3x3 grid of 24x24 warp tiles
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
+  // warp tile 24 (mi) x 72 (ni): warp row wm covers mo_l = wm / 3, mi 24 * (wm % 3) ..
+  const int wm = warp >> 1, wn = warp & 1;
+  const int mo_l = wm / 3, m0 = (wm % 3) * 24;
   const int qrow = lane >> 2, qk = lane & 3;
+  // A image [mo2][kB][mi][kA] (64-byte rows): swz64 XORs the 16-byte chunk with
+  // row bits 1..2 = qrow bits 1..2 (m0 and 8 i are multiples of 8);
+  // B image [no2][kA][ni][kB] (32-byte rows): swz32 XORs with row bit 2
+  const int a_lane = (mo_l * KB * EXT + m0 + qrow) * 64;
+  const int b_lane = (wn * KA * EXT + qrow) * 32;
+  const int sA = ((qrow >> 1) & 3) << 4, sB = ((qrow >> 2) & 1) << 4;
   // functional operands (aA x + bA)(aB y + bB): the K-sum is hoisted out of
   // the DMMA loop, C = aA aB S + aA bB rowA + bA aB rowB + bA bB |K|
   const bool affine = p.a_alpha >= 0 || p.b_alpha >= 0;
@@ -144,11 +158,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (std::int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     std::int64_t mo, no;
     tile_coords(t, mo, no);
-    double acc[3][3][2];
+    double acc[3][9][2];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < 9; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     for (std::int64_t ks = 0; ks < ksteps; ++ks, ++it) {
       const int s = static_cast<int>(it % S);
@@ -158,45 +172,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       const unsigned char* sb = sa + kTileBytes;
 #pragma unroll
       for (int kc = 0; kc < KT / 4; ++kc) {
-        // k chunk of 4 = {kB pair} x {kA pair}; lane's k = (e_l, f)
-        const int e_l = 2 * (kc >> 2) + (qk >> 1);
-        const int f = 2 * (kc & 3) + (qk & 1);
-        double af[3], bf[3];
+        // k chunk of 4: lane's k = (kB e_l, kA f) with f in {0,1,4,5} + 2 (kc >> 2)
+        // and e_l = qk ^ (kc & 3). A 64-bit fragment load is served per
+        // half-warp (4 rows x 4 k); this choice puts the 16 words of each half
+        // in 16 distinct bank pairs on both swizzled images (one wavefront per
+        // half, the minimum), and the 8 chunks cover the stage's 8 x 4 k.
+        const int e_l = qk ^ (kc & 3);
+        const int f = 2 * (kc >> 2) + (qk & 1) + 4 * (qk >> 1);
+        // the swizzle XOR only sees row bits (lane constants sA / sB), so each
+        // fragment is lane base + per-chunk k offset + an immediate
+        const unsigned char* pa = sa + a_lane + e_l * (EXT * 64) + ((f * 8) ^ sA);
+        const unsigned char* pb = sb + b_lane + f * (EXT * 32) + ((e_l * 8) ^ sB);
+        double af[3], bf[9];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          const int m = wm * 24 + i * 8 + qrow;
-          // A image [kB][mi][kA]: 8 rows x 16 B per kB plane -> 2 wavefronts (minimum)
-          af[i] = *reinterpret_cast<const double*>(sa + swz64(static_cast<std::uint32_t>(e_l * BM * 64 + m * 64 + f * 8)));
-        }
+        for (int i = 0; i < 3; ++i) af[i] = *reinterpret_cast<const double*>(pa + i * 8 * 64);
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const int n = wn * 24 + j * 8 + qrow;
-          // B image [kA][ni][kB]: same pattern with the roles of kA and kB swapped
-          bf[j] = *reinterpret_cast<const double*>(sb + swz64(static_cast<std::uint32_t>(f * BN * 64 + n * 64 + e_l * 8)));
-        }
+        for (int j = 0; j < 9; ++j) bf[j] = *reinterpret_cast<const double*>(pb + j * 8 * 32);
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-          for (int j = 0; j < 3; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < 9; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
     }
 
     // epilogue: fragment (row qrow, cols 2*qk, 2*qk+1) of each 8x8 block
-    double* cbase = p.C + mo * p.c_mo + no * p.c_no;
+    const std::int64_t gmo = mo * MT + mo_l, gno = no * NT + wn;
+    if (gmo >= p.ext_mo || gno >= p.ext_no) continue;
+    double* cbase = p.C + gmo * p.c_mo + gno * p.c_no;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const int m = wm * 24 + i * 8 + qrow;
+      const int m = m0 + i * 8 + qrow;
+      const double ra = (affine && bB != 0.0) ? p.rowA[gmo * p.ext_mi + m] : 0.0;
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const int n = wn * 24 + j * 8 + 2 * qk;
+      for (int j = 0; j < 9; ++j) {
+        const int n = j * 8 + 2 * qk;
         double* dst = cbase + m * p.c_mi + n * p.c_ni;
         if (affine) {
-          const double ra = (bB != 0.0) ? p.rowA[mo * p.ext_mi + m] : 0.0;
           const double k = bA * bB * p.kdim;
           for (int v = 0; v < 2; ++v) {
-            const double rb = (bA != 0.0) ? p.rowB[no * p.ext_ni + n + v] : 0.0;
+            const double rb = (bA != 0.0) ? p.rowB[gno * p.ext_ni + n + v] : 0.0;
             acc[i][j][v] = fma(aA * aB, acc[i][j][v], fma(aA * bB, ra, fma(bA * aB, rb, k)));
           }
         }
@@ -259,7 +275,7 @@ bool make_map(CUtensorMap* map, const double* base, const std::uint64_t dims[4],
 }  // namespace
 
 bool gett_supported(std::int64_t ext_mi, std::int64_t ext_ni, std::int64_t ext_ka, std::int64_t ext_kb) {
-  return ext_mi == BM && ext_ni == BN && ext_ka % KA == 0 && ext_kb % KB == 0;
+  return ext_mi == EXT && ext_ni == EXT && ext_ka % KA == 0 && ext_kb % KB == 0;
 }
 
 int launch_gett(const GettLaunch& L, void* stream) {
@@ -270,7 +286,7 @@ int launch_gett(const GettLaunch& L, void* stream) {
                                    static_cast<std::uint64_t>(L.ext_kb), static_cast<std::uint64_t>(L.ext_mo)};
     const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.a_mi), static_cast<std::uint64_t>(L.a_kb),
                                   static_cast<std::uint64_t>(L.a_mo)};
-    const std::uint32_t box[4] = {KA, BM, KB, 1};
+    const std::uint32_t box[4] = {KA, EXT, KB, MT};
     if (!make_map(&tmA, L.A, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
   }
   {
@@ -278,12 +294,14 @@ int launch_gett(const GettLaunch& L, void* stream) {
                                    static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_no)};
     const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.b_ni), static_cast<std::uint64_t>(L.b_ka),
                                   static_cast<std::uint64_t>(L.b_no)};
-    const std::uint32_t box[4] = {KB, BN, KA, 1};
-    if (!make_map(&tmB, L.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+    const std::uint32_t box[4] = {KB, EXT, KA, NT};
+    if (!make_map(&tmB, L.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_32B)) return cudaErrorInvalidValue;
   }
   GettDev d{};
-  d.mo = L.ext_mo;
-  d.no = L.ext_no;
+  d.mo = (L.ext_mo + MT - 1) / MT;
+  d.no = (L.ext_no + NT - 1) / NT;
+  d.ext_mo = L.ext_mo;
+  d.ext_no = L.ext_no;
   d.ka_steps = L.ext_ka / KA;
   d.kb_steps = L.ext_kb / KB;
   d.c_mo = L.c_mo;
@@ -311,7 +329,7 @@ int launch_gett(const GettLaunch& L, void* stream) {
         L.B, L.scratch + ra, L.ext_no, L.ext_ni, L.b_no, L.b_ni, L.ext_ka, L.ext_kb, L.b_ka, 1);
   }
   d.stages = L.stages > 0 ? L.stages : 3;
-  d.group = L.group > 0 ? L.group : 12;
+  d.group = L.group > 0 ? L.group : 6;
   const size_t smem = 1024 + static_cast<size_t>(d.stages) * 2 * kTileBytes + 16 * d.stages;
   cudaError_t e = cudaFuncSetAttribute(gett_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

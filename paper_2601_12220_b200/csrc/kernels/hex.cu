@@ -24,6 +24,8 @@
 // DMMA tiles (padding to 8x8 wastes 61%).
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "launch.h"
 #include "ptx.cuh"
 
@@ -280,6 +282,330 @@ __global__ void __launch_bounds__(kThreads, 2) hex_kernel(const __grid_constant_
   }
 }
 
+// ---------------------------------------------------------------- v2 -----
+// Constant-bank operators and ownership that matches each pass to its sweeps.
+//
+// The 1-D operators live in constant memory (staged per launch, stream-ordered)
+// and every sweep is unrolled for a compile-time (matrix, direction), so each
+// DFMA takes its coefficient straight from the constant bank: no operator
+// loads, no operator registers. Shared memory then only carries the three
+// unavoidable transposes per (element, field):
+//   A  plane j (k,l) of u, one direction y per warp:  F3[y] along l, F2[y] along k
+//   B  line (k,l) over j, two fields per thread:      F1[y] along j, q_x = G t_y,
+//                                                      B1[x]^T along a (G read once per two fields)
+//   C  plane i (b,c), one direction x per warp:       B2[x]^T along b, B3[x]^T along c
+//   S  row (i,m): y = sum_x partial_x, streamed to HBM
+// 3187 shared doubles per (element, field) against 12375 DFMA (v1: 5250 plus
+// operator loads). Work cubes (cube = field * 2 + element) sit 137 doubles
+// apart; with cube-fastest lanes in A and C and line-fastest lanes in B every
+// W access is conflict-free (two wavefronts per warp-wide 8-byte access);
+// only B's G reads keep a 2-way conflict where a half-warp spans both elements.
+__constant__ double c_hex_ops[6][ND][P2];
+// W cube stride: odd (plane accesses of cube-fastest lanes hit distinct banks)
+// and 9 mod 16 (consecutive lines of consecutive cubes continue the bank walk)
+constexpr int CS2 = 137;  // F1 F2 F3 B1 B2 B3, [d][o][i] as stored
+
+struct Hex2Dev {
+  std::int64_t E;
+  int rows;
+  const double* G;
+  const double* U[kMaxFields];
+  double* Y[kMaxFields];
+};
+
+// forward operator entry M[o][i] = F[o][i]; backward M[o][i] = B[i][o]
+template <int K, int D, bool kBack>
+__device__ __forceinline__ double cop(int o, int i) {
+  return kBack ? c_hex_ops[K][D][i * P + o] : c_hex_ops[K][D][o * P + i];
+}
+
+template <int K, int D, bool kBack>
+__device__ __forceinline__ void rows_c(double (&v)[P][P]) {
+#pragma unroll
+  for (int r = 0; r < P; ++r) {
+    double o[P];
+#pragma unroll
+    for (int a = 0; a < P; ++a) {
+      double s = cop<K, D, kBack>(a, 0) * v[r][0];
+#pragma unroll
+      for (int b = 1; b < P; ++b) s = fma(cop<K, D, kBack>(a, b), v[r][b], s);
+      o[a] = s;
+    }
+#pragma unroll
+    for (int a = 0; a < P; ++a) v[r][a] = o[a];
+  }
+}
+
+template <int K, int D, bool kBack>
+__device__ __forceinline__ void cols_c(double (&v)[P][P]) {
+#pragma unroll
+  for (int col = 0; col < P; ++col) {
+    double o[P];
+#pragma unroll
+    for (int a = 0; a < P; ++a) {
+      double s = cop<K, D, kBack>(a, 0) * v[0][col];
+#pragma unroll
+      for (int b = 1; b < P; ++b) s = fma(cop<K, D, kBack>(a, b), v[b][col], s);
+      o[a] = s;
+    }
+#pragma unroll
+    for (int a = 0; a < P; ++a) v[a][col] = o[a];
+  }
+}
+
+// pass A: u plane j -> t_y plane j (F3[y] along l, F2[y] along k)
+template <int Y>
+__device__ __forceinline__ void pass_a(const double* in, double* out) {
+  double v[P][P];
+#pragma unroll
+  for (int k = 0; k < P; ++k)
+#pragma unroll
+    for (int l = 0; l < P; ++l) v[k][l] = in[k * P + l];
+  rows_c<2, Y, false>(v);
+  cols_c<1, Y, false>(v);
+#pragma unroll
+  for (int b = 0; b < P; ++b)
+#pragma unroll
+    for (int c = 0; c < P; ++c) out[b * P + c] = v[b][c];
+}
+
+// pass C: q'_x plane i -> partial y_x plane i (B2[x]^T along b, B3[x]^T along c)
+template <int X>
+__device__ __forceinline__ void pass_c(double* io) {
+  double v[P][P];
+#pragma unroll
+  for (int b = 0; b < P; ++b)
+#pragma unroll
+    for (int c = 0; c < P; ++c) v[b][c] = io[b * P + c];
+  cols_c<4, X, true>(v);
+  rows_c<5, X, true>(v);
+#pragma unroll
+  for (int m = 0; m < P; ++m)
+#pragma unroll
+    for (int n = 0; n < P; ++n) io[m * P + n] = v[m][n];
+}
+
+// F1[y] along j on one line (y compile-time)
+template <int Y>
+__device__ __forceinline__ void line_f1(double (&t)[P]) {
+  double o[P];
+#pragma unroll
+  for (int a = 0; a < P; ++a) {
+    double s = cop<0, Y, false>(a, 0) * t[0];
+#pragma unroll
+    for (int j = 1; j < P; ++j) s = fma(cop<0, Y, false>(a, j), t[j], s);
+    o[a] = s;
+  }
+#pragma unroll
+  for (int a = 0; a < P; ++a) t[a] = o[a];
+}
+
+// B1[x]^T along a on one line, stored with stride P2
+template <int X>
+__device__ __forceinline__ void line_b1(const double (&t)[P], double* out) {
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    double s = cop<3, X, true>(i, 0) * t[0];
+#pragma unroll
+    for (int a = 1; a < P; ++a) s = fma(cop<3, X, true>(i, a), t[a], s);
+    out[i * P2] = s;
+  }
+}
+
+// pass B on line (k,l) of NF fields: wl[f] = W + cube*P3 + kl (direction 0),
+// direction stride ds; g = Gs + el*P3 + kl with (x,y) block stride gs
+template <int NF>
+__device__ __forceinline__ void pass_b(double* const (&wl)[NF], int ds, const double* g, int gs) {
+  double t[NF][ND][P];
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int y = 0; y < ND; ++y)
+#pragma unroll
+      for (int j = 0; j < P; ++j) t[f][y][j] = wl[f][y * ds + j * P2];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    line_f1<0>(t[f][0]);
+    line_f1<1>(t[f][1]);
+    line_f1<2>(t[f][2]);
+  }
+  // q_x = sum_y G[x,y] t_y, pointwise; G read once for all NF fields
+#pragma unroll
+  for (int a = 0; a < P; ++a) {
+    double gv[ND][ND];
+#pragma unroll
+    for (int x = 0; x < ND; ++x)
+#pragma unroll
+      for (int y = 0; y < ND; ++y) gv[x][y] = g[(x * ND + y) * gs + a * P2];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      double q[ND];
+#pragma unroll
+      for (int x = 0; x < ND; ++x) {
+        double s = gv[x][0] * t[f][0][a];
+        s = fma(gv[x][1], t[f][1][a], s);
+        q[x] = fma(gv[x][2], t[f][2][a], s);
+      }
+#pragma unroll
+      for (int x = 0; x < ND; ++x) t[f][x][a] = q[x];
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    line_b1<0>(t[f][0], wl[f]);
+    line_b1<1>(t[f][1], wl[f] + ds);
+    line_b1<2>(t[f][2], wl[f] + 2 * ds);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) hex2_kernel(const __grid_constant__ Hex2Dev p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  const int R = p.rows;
+  const int nblk = NE * R;   // cubes per pair, cube = field * NE + element
+  const int ds = nblk * CS2;  // direction stride in W
+  // layout (doubles): Gs[9][NE*P3] | Us[R][NE*P3] | W[ND][nblk][CS2] | mbar {G, U}
+  double* Gs = sm;
+  double* Us = Gs + ND * ND * NE * P3;
+  double* W = Us + R * NE * P3;
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(W + ND * ds);
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+
+  const std::int64_t npairs = p.E / NE;
+  const std::uint32_t bytes = static_cast<std::uint32_t>(NE * P3 * 8);
+  auto issue_g = [&](std::int64_t pair) {
+    ptx::mbar_arrive_expect_tx(&bar[0], bytes * static_cast<std::uint32_t>(ND * ND));
+    const std::int64_t e0 = pair * NE;
+    for (int xy = 0; xy < ND * ND; ++xy)
+      ptx::bulk_g2s(Gs + xy * NE * P3, p.G + (xy * p.E + e0) * P3, bytes, &bar[0]);
+  };
+  auto issue_u = [&](std::int64_t pair) {
+    ptx::mbar_arrive_expect_tx(&bar[1], bytes * static_cast<std::uint32_t>(R));
+    const std::int64_t e0 = pair * NE;
+    for (int f = 0; f < R; ++f) ptx::bulk_g2s(Us + f * NE * P3, p.U[f] + e0 * P3, bytes, &bar[1]);
+  };
+  if (threadIdx.x == 0 && blockIdx.x < npairs) {
+    issue_u(blockIdx.x);
+    issue_g(blockIdx.x);
+  }
+
+  // passes A and C: thread -> (direction, cube, plane), direction slowest, so
+  // only the warps straddling a direction boundary run two code paths
+  const int dir = threadIdx.x / (nblk * P);
+  const int ptask = threadIdx.x - dir * nblk * P;
+  const bool pactive = dir < ND;
+  const int pplane = ptask / nblk, pcube = ptask - pplane * nblk;  // cube fastest
+  const double* a_in = Us + pcube * P3 + pplane * P2;
+  double* a_out = W + dir * ds + pcube * CS2 + pplane * P2;
+  // pass B: thread -> (line, element, field pair (f, f + H)), line fastest
+  const int H = (R + 1) / 2;
+  const int nbt = H * NE * P2;
+
+  int it = 0;
+  for (std::int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x, ++it) {
+    const std::uint32_t phase = static_cast<std::uint32_t>(it & 1);
+    const bool more = pair + gridDim.x < npairs;
+
+    ptx::mbar_wait(&bar[1], phase);
+    if (pactive) {
+      if (dir == 0) pass_a<0>(a_in, a_out);
+      else if (dir == 1) pass_a<1>(a_in, a_out);
+      else pass_a<2>(a_in, a_out);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && more) issue_u(pair + gridDim.x);
+
+    ptx::mbar_wait(&bar[0], phase);
+    for (int t = threadIdx.x; t < nbt; t += blockDim.x) {
+      const int kl = t % P2;
+      const int r = t / P2;
+      const int el = r % NE, f0 = r / NE, f1 = f0 + H;
+      const double* g = Gs + el * P3 + kl;
+      if (f1 < R) {
+        double* const wl[2] = {W + (f0 * NE + el) * CS2 + kl, W + (f1 * NE + el) * CS2 + kl};
+        pass_b<2>(wl, ds, g, NE * P3);
+      } else {
+        double* const wl[1] = {W + (f0 * NE + el) * CS2 + kl};
+        pass_b<1>(wl, ds, g, NE * P3);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && more) issue_g(pair + gridDim.x);
+
+    if (pactive) {
+      if (dir == 0) pass_c<0>(a_out);
+      else if (dir == 1) pass_c<1>(a_out);
+      else pass_c<2>(a_out);
+    }
+    __syncthreads();
+
+    const std::int64_t e0 = pair * NE;
+    // y rows of a field are one contiguous run of NE * P3 doubles: coalesced
+    for (int off = threadIdx.x; off < NE * P3; off += blockDim.x) {
+      const int el = off / P3;
+      const double* w = W + el * CS2 + (off - el * P3);
+#pragma unroll
+      for (int f = 0; f < kMaxFields; ++f)
+        if (f < R) __stcs(p.Y[f] + e0 * P3 + off, (w[f * NE * CS2] + w[ds + f * NE * CS2]) + w[2 * ds + f * NE * CS2]);
+    }
+    __syncthreads();  // W is rewritten by the next pair's pass A
+  }
+}
+
+// The operator constants are shared by every launch on a device: a launch
+// waits for the previous one (any stream) before restaging them.
+struct HexConstSlot {
+  cudaEvent_t last = nullptr;
+};
+std::mutex g_hex_mu;
+HexConstSlot g_hex_slot[64];
+
+int launch_hex2(const HexLaunch& L, cudaStream_t st) {
+  const int R = L.rows;
+  const int nblk = NE * R;
+  const int threads = kThreads;  // >= ND * nblk * P plane tasks for R <= 8
+  Hex2Dev d{};
+  d.E = L.E;
+  d.rows = R;
+  d.G = L.G;
+  for (int f = 0; f < R; ++f) {
+    d.U[f] = L.U[f];
+    d.Y[f] = L.Y[f];
+  }
+  const size_t doubles = ND * ND * NE * P3 + R * NE * P3 + ND * nblk * CS2;
+  const size_t smem = doubles * 8 + 16;
+  cudaError_t e = cudaFuncSetAttribute(hex2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(hex2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  device_sm_count(&sms);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hex2_kernel, threads, smem);
+  std::int64_t grid = static_cast<std::int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+  if (grid > L.E / NE) grid = L.E / NE;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_hex_mu);
+  HexConstSlot& slot = g_hex_slot[dev & 63];
+  if (slot.last) cudaStreamWaitEvent(st, slot.last, 0);
+  else if ((e = cudaEventCreateWithFlags(&slot.last, cudaEventDisableTiming)) != cudaSuccess) return e;
+  for (int k = 0; k < 6; ++k) {
+    e = cudaMemcpyToSymbolAsync(c_hex_ops, L.mats[k], ND * P2 * sizeof(double), k * ND * P2 * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+  }
+  hex2_kernel<<<static_cast<int>(grid), threads, smem, st>>>(d);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cudaEventRecord(slot.last, st);
+}
+
 }  // namespace
 
 bool hex_supported(int nd, int p, std::int64_t E, int rows) {
@@ -289,6 +615,7 @@ bool hex_supported(int nd, int p, std::int64_t E, int rows) {
 int launch_hex(const HexLaunch& L, void* stream) {
   if (!hex_supported(L.ND, L.P, L.E, L.rows)) return cudaErrorInvalidValue;
   if (L.E == 0) return cudaSuccess;
+  if (L.variant != 1) return launch_hex2(L, static_cast<cudaStream_t>(stream));
   HexDev d{};
   d.E = L.E;
   d.rows = L.rows;

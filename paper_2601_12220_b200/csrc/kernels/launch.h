@@ -249,6 +249,7 @@ struct HexLaunch {
   const double* G;        // [ND, ND, E, P, P, P]
   const double* U[8];
   double* Y[8];
+  int variant;  // 2: constant-bank operators, plane/line passes (default); 1: register-plane passes
 };
 
 int launch_hex(const HexLaunch& p, void* stream);

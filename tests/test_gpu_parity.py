@@ -346,12 +346,15 @@ def test_tensor_train_f32_tensor_cores(fe, torch_cuda, n, meta):
     assert err <= max(1e-5, 4 * err_f32), (err, err_f32)
 
 
-def test_hex_sumfact_small(fe, ref, torch_cuda):
-    """C2's sum-factorised operator at oracle-sized extents."""
+@pytest.mark.parametrize("meta", ["", "v=1"])
+def test_hex_sumfact_small(fe, ref, torch_cuda, meta):
+    """C2's sum-factorised operator at oracle-sized extents, both kernel
+    variants, with shared (A_d) and six distinct forward/backward operators."""
     from paper_2601_12220_b200 import configs as C
-    for E, b in [(2, 1), (4, 3)]:
-        e = C.hex_poisson(E=E, b=b)
-        plan = fe.Plan(einsum=e)
+    for E, b, distinct in [(2, 1, False), (4, 3, False), (2, 8, True), (6, 5, True)]:
+        e = C.hex_poisson(E=E, b=b, distinct=distinct)
+        opts = {"meta": meta, "transform": "hex_sumfact/v1"} if meta else None
+        plan = fe.Plan(einsum=e, options=opts) if opts else fe.Plan(einsum=e)
         assert plan.info["transform"] == "hex_sumfact/v1"
         bind = ref.random_bindings(e, E + b)
         got = run_plan(torch_cuda, plan, bind)

@@ -30,7 +30,6 @@ namespace {
 
 constexpr int R = 64;                  // core size
 constexpr int kConsumerWarps = 8;      // 8 warps x (32 x 32) per GEMM
-constexpr int kThreads = 32 * (kConsumerWarps + 1);
 constexpr int kPair = 2;               // samples per iteration
 
 __device__ __forceinline__ std::uint32_t swz(std::uint32_t off) { return off ^ (((off >> 7) & 7u) << 4); }
@@ -52,6 +51,35 @@ __device__ __forceinline__ double ld(const unsigned char* base, int r, int c) {
   return static_cast<double>(*reinterpret_cast<const T*>(base + Panels<T>::off(r, c)));
 }
 
+// Fragment addressing. A DMMA k-chunk gives lane (qr, qk) row r = r0 + 8 a + qr
+// and column k = k0 + (qk & 1) + 8 (qk >> 1), k0 in {0, 2, 4, 6} + 16 q: a
+// 64-bit load is served per half-warp (4 rows x 4 k), and against the 128B
+// swizzle (16-byte chunk ^= r & 7) these k spread each half over all 32 banks
+// (adjacent k pairs would hit the same chunks for rows qr and qr ^ 1). The qk
+// and k0 parts of the column byte offset occupy disjoint bits, so the address
+// splits into a lane base + a per-chunk offset + the immediate 1024 a.
+template <typename T>
+struct Frag {
+  static constexpr int P = Panels<T>::P;
+  // bits of the column byte offset owned by qk: double 3 and 6, float 2 and 5
+  static constexpr std::uint32_t kQMask = sizeof(T) == 8 ? 0x48u : 0x24u;
+  __device__ static std::uint32_t lane(int r0, int qr, int qk) {
+    const std::uint32_t sx = static_cast<std::uint32_t>(qr) << 4;
+    const std::uint32_t q = static_cast<std::uint32_t>((qk & 1) + 8 * (qk >> 1)) * sizeof(T);
+    return static_cast<std::uint32_t>((r0 + qr) * 128) + (q ^ (sx & kQMask));
+  }
+  __device__ static std::uint32_t kofs(int k0, int qr) {
+    const std::uint32_t sx = static_cast<std::uint32_t>(qr) << 4;
+    return static_cast<std::uint32_t>((k0 / P) * Panels<T>::kPanelBytes) +
+           ((static_cast<std::uint32_t>(k0 % P) * sizeof(T)) ^ (sx & ~kQMask & 0x70u));
+  }
+  __device__ static double at(const unsigned char* p, int a) {
+    return static_cast<double>(*reinterpret_cast<const T*>(p + a * 8 * 128));
+  }
+};
+// k0 of chunk kp (16 chunks of 4 cover k = 0..63)
+__device__ __forceinline__ int chunk_k0(int kp) { return (kp >> 2) * 16 + (kp & 3) * 2; }
+
 struct TTDev {
   std::int64_t nb;
   const void* G1;
@@ -60,73 +88,86 @@ struct TTDev {
   std::int64_t y_sn;  // Y sample stride (elements); rows are i*64 + k
 };
 
+// Warp groups of 8 DMMA warps, each with its own single X stage, run
+// independent sample pairs (fp64: two groups, 16 warps = four per SM
+// sub-partition); while one group waits at its barriers or for its next X
+// pair, the other keeps the tensor pipe busy. Warp 0 of a group issues the
+// group's TMA once the group has released its stage.
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1)
+struct TTShape {
+  static constexpr bool kInPlaceT = sizeof(T) == 8;  // T^T overwrites the consumed X stage
+  static constexpr int kGroups = sizeof(T) == 8 ? 2 : 1;
+  static constexpr int kStageBytes = kPair * Panels<T>::kBytes;
+  static constexpr int kGroupBytes = kStageBytes + (kInPlaceT ? 0 : kPair * Panels<double>::kBytes);
+  static constexpr int kThreadsT = 32 * kConsumerWarps * kGroups;
+  static constexpr size_t kSmem = 1024 + 2 * Panels<double>::kBytes + static_cast<size_t>(kGroups) * kGroupBytes + 64;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(TTShape<T>::kThreadsT, 1)
     tt_kernel(const __grid_constant__ TTDev p, const __grid_constant__ CUtensorMap tmX) {
   using PT = Panels<T>;
   using PD = Panels<double>;
-  constexpr bool kInPlaceT = sizeof(T) == 8;       // T^T overwrites the consumed X stage
-  constexpr int kStageBytes = kPair * PT::kBytes;
+  using SH = TTShape<T>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
   unsigned char* g1 = base;                          // G1 [i][j] fp64 panels
   unsigned char* g2 = g1 + PD::kBytes;               // G2 [k][l] fp64 panels
-  unsigned char* xr = g2 + PD::kBytes;               // 2 stages x 2 samples of X
-  unsigned char* tbuf = xr + 2 * kStageBytes;        // fp32 only: T^T for 2 samples
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(tbuf + (kInPlaceT ? 0 : kPair * PD::kBytes));
-  std::uint64_t* empty = full + 2;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(g2 + PD::kBytes + SH::kGroups * SH::kGroupBytes);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp / kConsumerWarps, wl = warp % kConsumerWarps;
+  unsigned char* xs0 = g2 + PD::kBytes + grp * SH::kGroupBytes;  // this group's X pair
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], kConsumerWarps);
-    }
+    for (int g = 0; g < SH::kGroups; ++g) ptx::mbar_init(&full[g], 1);
     ptx::fence_barrier_init();
   }
+  __syncthreads();
+
+  const std::int64_t npairs = (p.nb + kPair - 1) / kPair;
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * SH::kGroups;
+  const bool leader = wl == 0 && lane == 0;
+  auto issue = [&](std::int64_t pr) {
+    ptx::mbar_arrive_expect_tx(&full[grp], SH::kStageBytes);
+    for (int smp = 0; smp < kPair; ++smp)
+      for (int panel = 0; panel < R / PT::P; ++panel) {
+        unsigned char* dst = xs0 + smp * PT::kBytes + panel * PT::kPanelBytes;
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+                ptx::smem_addr(dst)),
+            "l"(&tmX), "r"(ptx::smem_addr(&full[grp])), "r"(panel * PT::P), "r"(0),
+            "r"(static_cast<int>(pr * kPair + smp))
+            : "memory");
+      }
+  };
+  const std::int64_t first = static_cast<std::int64_t>(blockIdx.x) * SH::kGroups + grp;
+  if (leader && first < npairs) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    issue(first);
+  }
+  // G1/G2 staged (as fp64 panels) while the first X pairs are in flight
   for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
     const int r = t / R, c = t % R;
     *reinterpret_cast<double*>(g1 + PD::off(r, c)) = static_cast<double>(static_cast<const T*>(p.G1)[t]);
     *reinterpret_cast<double*>(g2 + PD::off(r, c)) = static_cast<double>(static_cast<const T*>(p.G2)[t]);
   }
   __syncthreads();
-
-  const std::int64_t npairs = (p.nb + kPair - 1) / kPair;
-  if (warp == kConsumerWarps) {
-    if (lane != 0) return;
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
-    int it = 0;
-    for (std::int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
-      const int s = it & 1;
-      ptx::mbar_wait(&empty[s], ((it >> 1) & 1u) ^ 1u);
-      ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
-      for (int smp = 0; smp < kPair; ++smp)
-        for (int panel = 0; panel < R / PT::P; ++panel) {
-          unsigned char* dst = xr + s * kStageBytes + smp * PT::kBytes + panel * PT::kPanelBytes;
-          asm volatile(
-              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
-                  ptx::smem_addr(dst)),
-              "l"(&tmX), "r"(ptx::smem_addr(&full[s])), "r"(panel * PT::P), "r"(0),
-              "r"(static_cast<int>(pr * kPair + smp))
-              : "memory");
-        }
-    }
-    return;
-  }
+  auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kConsumerWarps * 32) : "memory"); };
 
   const int qr = lane >> 2, qk = lane & 3;
   // GEMM 1 tile: stacked rows [32*(w/2), +32) (sample (w/2)/2), cols [32*(w%2), +32)
-  const int smp = warp >> 2;
-  const int r1 = (warp >> 1) * 32 - smp * R, c1 = (warp & 1) * 32;
+  const int smp = wl >> 2;
+  const int r1 = (wl >> 1) * 32 - smp * R, c1 = (wl & 1) * 32;
   // GEMM 2 tile (same sample): rows i [32*(w%2), +32), cols k [32*((w>>1)&1), +32)
-  const int r2 = (warp & 1) * 32, c2 = ((warp >> 1) & 1) * 32;
+  const int r2 = (wl & 1) * 32, c2 = ((wl >> 1) & 1) * 32;
+  const std::uint32_t a1_lane = Frag<T>::lane(r1, qr, qk), b1_lane = Frag<double>::lane(c1, qr, qk);
+  const std::uint32_t a2_lane = Frag<double>::lane(r2, qr, qk), b2_lane = Frag<double>::lane(c2, qr, qk);
+  unsigned char* xs = xs0 + smp * PT::kBytes;
+  unsigned char* ts = SH::kInPlaceT ? xs : xs0 + SH::kStageBytes + smp * PD::kBytes;
   int it = 0;
-  for (std::int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++it) {
-    const int s = it & 1;
-    ptx::mbar_wait(&full[s], (it >> 1) & 1u);
-    unsigned char* xs = xr + s * kStageBytes + smp * PT::kBytes;
-    unsigned char* ts = kInPlaceT ? xs : tbuf + smp * PD::kBytes;
+  for (std::int64_t pr = first; pr < npairs; pr += stride, ++it) {
+    ptx::mbar_wait(&full[grp], it & 1u);
 
     double acc[4][4][2];
 #pragma unroll
@@ -134,20 +175,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     // GEMM 1: T[j,k] = sum_l X[j,l] G2[k,l]
-#pragma unroll 2
-    for (int k0 = 0; k0 < R; k0 += 4) {
+#pragma unroll 4
+    for (int kp = 0; kp < R / 4; ++kp) {
+      const int k0 = chunk_k0(kp);
       double af[4], bf[4];
+      const unsigned char* pa = xs + a1_lane + Frag<T>::kofs(k0, qr);
+      const unsigned char* pb = g2 + b1_lane + Frag<double>::kofs(k0, qr);
 #pragma unroll
-      for (int a = 0; a < 4; ++a) af[a] = ld<T>(xs, r1 + a * 8 + qr, k0 + qk);
+      for (int a = 0; a < 4; ++a) af[a] = Frag<T>::at(pa, a);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = ld<double>(g2, c1 + b * 8 + qr, k0 + qk);
+      for (int b = 0; b < 4; ++b) bf[b] = Frag<double>::at(pb, b);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) ptx::dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
     // all X of the pair consumed before T^T may overwrite it
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    group_sync();
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -157,28 +201,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int j = r1 + a * 8 + qr, k = c1 + b * 8 + 2 * qk + v;
           *reinterpret_cast<double*>(ts + PD::off(k, j)) = acc[a][b][v];
         }
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    group_sync();
 
     // GEMM 2: Y[i,k] = sum_j G1[i,j] T[j,k]
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll 2
-    for (int k0 = 0; k0 < R; k0 += 4) {
+#pragma unroll 4
+    for (int kp = 0; kp < R / 4; ++kp) {
+      const int k0 = chunk_k0(kp);
       double af[4], bf[4];
+      const std::uint32_t ko = Frag<double>::kofs(k0, qr);
+      const unsigned char* pa = g1 + a2_lane + ko;
+      const unsigned char* pb = ts + b2_lane + ko;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) af[a] = ld<double>(g1, r2 + a * 8 + qr, k0 + qk);
+      for (int a = 0; a < 4; ++a) af[a] = Frag<double>::at(pa, a);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = ld<double>(ts, c2 + b * 8 + qr, k0 + qk);
+      for (int b = 0; b < 4; ++b) bf[b] = Frag<double>::at(pb, b);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) ptx::dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    // the stage (X, and T^T when in place) is free once every warp has read it
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    // the group's stage (X, and T^T when in place) is free once every warp of
+    // the group has read it: refill it while the Y tiles drain
+    group_sync();
+    if (leader && pr + stride < npairs) issue(pr + stride);
 
     const std::int64_t n = pr * kPair + smp;
     if (n < p.nb) {
@@ -235,18 +284,15 @@ int launch_t(const TTLaunch& L, cudaStream_t stream) {
   d.G2 = L.G2;
   d.Y = L.Y;
   d.y_sn = L.y_sn;
-  constexpr bool kInPlaceT = sizeof(T) == 8;
-  const size_t smem = 1024 + 2 * PD::kBytes + 2 * kPair * PT::kBytes + (kInPlaceT ? 0 : kPair * PD::kBytes) + 64;
+  const size_t smem = TTShape<T>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(tt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int sms = 148;
   device_sm_count(&sms);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tt_kernel<T>, kThreads, smem);
   const std::int64_t npairs = (L.Nb + kPair - 1) / kPair;
-  std::int64_t grid = static_cast<std::int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
-  if (grid > npairs) grid = npairs;
-  tt_kernel<T><<<static_cast<int>(grid), kThreads, smem, stream>>>(d, tm);
+  std::int64_t grid = (npairs + TTShape<T>::kGroups - 1) / TTShape<T>::kGroups;
+  if (grid > sms) grid = sms;
+  tt_kernel<T><<<static_cast<int>(grid), TTShape<T>::kThreadsT, smem, stream>>>(d, tm);
   return cudaGetLastError();
 }
 

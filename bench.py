@@ -7,7 +7,8 @@ batched-einsum suite of BASELINE.json, on 1-8 B200s.
 
 A step evaluates every config of the suite once (one plan execution each).
 Inputs are synthetic dyadic values generated on the device; every config is
-preceded by an L2 flush (writes > 126 MB) and timed alone with CUDA events on
+preceded by an L2 flush (256 MiB written, then read back so the L2 is
+also clean) and timed alone with CUDA events on
 the launching stream; per-config times are max-reduced over ranks. FLOPs are
 the algorithmic (optimal pairwise contraction path) counts, operand FLOPs of
 functional operands included.
@@ -329,7 +330,7 @@ def gpu_arm(args):
             "dtype": "f64 (C4-f32: f32)", "data": "synthetic dyadic values m/2^19-1 generated on device",
             "config": {"workload": "TCCG+FEM suite " + ",".join(w.name for w in loads),
                        "suite": {n: CONFIG_DOC[n] for n in names}, "per_config": per, "skipped": skipped,
-                       "l2": "flushed (256 MiB write) before every config launch",
+                       "l2": "flushed before every config launch: 256 MiB write, then the same 256 MiB read back (L2 cold for the inputs and clean)",
                        "parallelism": f"dp{world} (element/batch-axis shards, no collective)",
                        "wall_s_timed_region": wall},
             "roofline": roof, "fp64_peak_tflops": fp64, "clocks": clocks.summary(),

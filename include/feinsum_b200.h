@@ -124,7 +124,8 @@ int fe_plan_destroy(fe_plan_t plan);
 /* deterministic dyadic values m/2^19 - 1 (the reference's random_bindings
  * value grid) written on the device */
 int fe_fill_dyadic(void* d_ptr, int storage, int64_t count, uint64_t seed, void* stream);
-/* overwrite `bytes` of scratch (>= L2 size) to evict L2 between timed runs */
+/* overwrite `bytes` of scratch (>= L2 size), then read it back, to evict L2
+ * between timed runs and leave it clean */
 int fe_flush_l2(void* d_scratch, int64_t bytes, void* stream);
 int fe_sm_count(void);
 /* measured FP64 throughput of the current device, TFLOP/s: which = 0 DFMA,

@@ -48,7 +48,11 @@ constexpr int kKBlockB = 2 * R * 128;        // 16 KB
 constexpr int kEpiWarps = 16;                // 4 column groups x 4 TMEM lane quarters
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = kEpiThreads + 32;
-constexpr std::uint32_t kTmemCols = 512;     // D1[2] + D2[2], 128 columns each
+constexpr std::uint32_t kTmemCols = 512;
+// TMEM columns: D1[2] (64 each), D2[2] (128 each), X hi / lo (A of GEMM1, 64 each)
+__host__ __device__ constexpr std::uint32_t d1_col(int b) { return static_cast<std::uint32_t>(b * 64); }
+__host__ __device__ constexpr std::uint32_t d2_col(int b) { return static_cast<std::uint32_t>(128 + b * 128); }
+constexpr std::uint32_t kXhCol = 384, kXlCol = 448;
 // instruction descriptor: D f32, A/B tf32, K-major both, M = 128, N = n
 constexpr std::uint32_t idesc(std::uint32_t n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
@@ -95,6 +99,15 @@ __device__ __forceinline__ void mma_tf32(std::uint32_t tmem, std::uint64_t da, s
       "l"(da), "l"(db), "r"(id), "r"(acc));
 }
 
+// A from TMEM (columns a_tmem .. +8: one K8 step, row = lane), B from shared memory
+__device__ __forceinline__ void mma_tf32_ts(std::uint32_t tmem, std::uint32_t a_tmem, std::uint64_t db, std::uint32_t id,
+                                            std::uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+      "r"(a_tmem), "l"(db), "r"(id), "r"(acc));
+}
+
 __device__ __forceinline__ void mma_commit(std::uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(ptx::smem_addr(bar))
                : "memory");
@@ -113,6 +126,16 @@ __device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, std::uint32_t (&v
 }
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// 32 lanes x 16 consecutive 32-bit columns, registers -> TMEM
+__device__ __forceinline__ void tmem_st16(std::uint32_t taddr, const std::uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -142,6 +165,27 @@ __device__ __forceinline__ void gemm3(std::uint32_t d, const unsigned char* ah, 
   }
 }
 
+// GEMM1 with A (X hi / lo) in TMEM: three N = 64 products accumulated in one
+// 64-column D1, small terms first: Xl G2h^T, Xh G2l^T, Xh G2h^T. B reads are
+// the only shared-memory traffic of the MMA (2 KB per instruction).
+__device__ __forceinline__ void gemm1_ts(std::uint32_t d, std::uint32_t xh, std::uint32_t xl, const unsigned char* g2) {
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    const int kb = ks >> 2, kin = (ks & 3) * 32;
+    mma_tf32_ts(d, xl + ks * 8, sdesc(g2 + kb * kKBlockB + kin), idesc(64), ks != 0);
+  }
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    const int kb = ks >> 2, kin = (ks & 3) * 32;
+    mma_tf32_ts(d, xh + ks * 8, sdesc(g2 + kb * kKBlockB + R * 128 + kin), idesc(64), 1);
+  }
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    const int kb = ks >> 2, kin = (ks & 3) * 32;
+    mma_tf32_ts(d, xh + ks * 8, sdesc(g2 + kb * kKBlockB + kin), idesc(64), 1);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     tt_tc_kernel(const __grid_constant__ TTTcDev p, const __grid_constant__ CUtensorMap tmX) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -149,11 +193,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
   unsigned char* g2 = base;  // [G2 hi ; G2 lo], B of GEMM1
   unsigned char* g1 = base + kG;  // [G1 hi ; G1 lo], B of GEMM2
-  unsigned char* xs0 = base + 2 * kG;   // X pair tiles (double-buffered); hi in place after the split
-  unsigned char* ls = xs0 + 2 * kTile;  // X lo
-  unsigned char* a2h = ls + kTile;      // T^T hi / lo
-  unsigned char* a2l = a2h + kTile;
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(a2l + kTile);
+  unsigned char* xs0 = base + 2 * kG;  // X pair tile (split into TMEM hi / lo, then refilled)
+  unsigned char* a2 = xs0 + kTile;     // T^T [2 buffers][hi, lo]: B of GEMM2(t) while epilogue 1 fills t+1
+  auto a2h = [&](int b) { return a2 + b * 2 * kTile; };
+  auto a2l = [&](int b) { return a2 + b * 2 * kTile + kTile; };
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(a2 + 4 * kTile);
   std::uint64_t* x_full = bars;         // [2]
   std::uint64_t* d1_full = bars + 2;    // [2]
   std::uint64_t* d2_full = bars + 4;    // [2]
@@ -209,36 +253,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
       auto tma_x = [&](std::int64_t t) {
-        const int b = static_cast<int>(t & 1);
         const int row0 = static_cast<int>((blockIdx.x + t * gridDim.x) * kRows);
-        unsigned char* xs = xs0 + b * kTile;
-        ptx::mbar_arrive_expect_tx(&x_full[b], kTile);
-        tma_2d(xs, &tmX, &x_full[b], 0, row0);
-        tma_2d(xs + kKBlockA, &tmX, &x_full[b], 32, row0);
+        ptx::mbar_arrive_expect_tx(&x_full[0], kTile);
+        tma_2d(xs0, &tmX, &x_full[0], 0, row0);
+        tma_2d(xs0 + kKBlockA, &tmX, &x_full[0], 32, row0);
       };
       auto gemm1 = [&](std::int64_t t) {
         const int b = static_cast<int>(t & 1);
         ptx::mbar_wait(lo_ready, static_cast<std::uint32_t>(t & 1));
         TT_TRACE(t, 0)
+        // split(t) has read the X tile: load X(t+1); it lands long before
+        // split(t+1), which follows GEMM1(t)
+        if (t + 1 < T) tma_x(t + 1);
         if (t >= 2) ptx::mbar_wait(&d1_free[b], static_cast<std::uint32_t>((t >> 1) - 1) & 1u);
         tc_after();
-        gemm3(tmem + static_cast<std::uint32_t>(b * 256), xs0 + b * kTile, ls, g2);
+        gemm1_ts(tmem + d1_col(b), tmem + kXhCol, tmem + kXlCol, g2);
         mma_commit(&d1_full[b]);
         TT_TRACE(t, 1)
       };
       if (T > 0) tma_x(0);
-      if (T > 1) tma_x(1);
       if (T > 0) gemm1(0);
       for (std::int64_t t = 0; t < T; ++t) {
         const int b = static_cast<int>(t & 1);
         // GEMM1(t+1) first: it runs while the epilogue warps turn T(t) into T^T
         if (t + 1 < T) gemm1(t + 1);
-        ptx::mbar_wait(a2_ready, static_cast<std::uint32_t>(t & 1));  // implies GEMM1(t) done: X tile b free
+        ptx::mbar_wait(a2_ready, static_cast<std::uint32_t>(t & 1));
         TT_TRACE(t, 2)
-        if (t + 2 < T) tma_x(t + 2);
         if (t >= 2) ptx::mbar_wait(&d2_free[b], static_cast<std::uint32_t>((t >> 1) - 1) & 1u);
         tc_after();
-        gemm3(tmem + static_cast<std::uint32_t>(b * 256 + 128), a2h, a2l, g1);
+        gemm3(tmem + d2_col(b), a2h(b), a2l(b), g1);
         mma_commit(&d2_full[b]);
         TT_TRACE(t, 3)
       }
@@ -248,22 +291,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warp = (column group cg, TMEM lane quarter q): rows q*32 + lane, 16 columns
     const int q = warp & 3, cg = warp >> 2;
     const int row = q * 32 + lane;
-    const std::uint32_t tl = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(cg * 16);
+    const std::uint32_t tl_row = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + static_cast<std::uint32_t>(cg * 16);
+    const std::uint32_t tl = tl_row;
+    // split: X rows from the TMA tile (thread = row, 16 columns l of its warp's
+    // column group, four 16-byte loads) into TMEM hi / lo, the A operand of
+    // GEMM1. The caller has seen GEMM1(t-1) complete (TMEM X free).
     auto split = [&](std::int64_t t) {
       const int b = static_cast<int>(t & 1);
-      ptx::mbar_wait(&x_full[b], static_cast<std::uint32_t>(t >> 1) & 1u);
+      ptx::mbar_wait(&x_full[0], static_cast<std::uint32_t>(t & 1));
       if (tid == 0) TT_TRACE(t, 9)
-      float4* xs = reinterpret_cast<float4*>(xs0 + b * kTile);
-      float4* lo = reinterpret_cast<float4*>(ls);
+      const unsigned char* xs = xs0 + (cg >> 1) * kKBlockA + row * 128;
+      std::uint32_t h[16], l[16];
 #pragma unroll
-      for (int k = 0; k < kTile / 16 / kEpiThreads; ++k) {
-        const int qd = tid + k * kEpiThreads;
-        const float4 x = xs[qd];
-        const float4 h = make_float4(hi_of(x.x), hi_of(x.y), hi_of(x.z), hi_of(x.w));
-        xs[qd] = h;
-        lo[qd] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int chunk = ((cg & 1) * 4 + c4) ^ (row & 7);
+        const float4 x = *reinterpret_cast<const float4*>(xs + chunk * 16);
+        const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float hv = hi_of(xv[e]);
+          h[c4 * 4 + e] = __float_as_uint(hv);
+          l[c4 * 4 + e] = __float_as_uint(xv[e] - hv);
+        }
       }
-      ptx::fence_proxy_async();
+      tmem_st16(tl_row + kXhCol, h);
+      tmem_st16(tl_row + kXlCol, l);
+      tmem_wait_st();
+      tc_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(lo_ready);
       if (tid == 0) TT_TRACE(t, 6)
@@ -272,8 +326,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto epi2 = [&](std::int64_t t1) {
       const int b1 = static_cast<int>(t1 & 1);
       std::uint32_t v[16], w[16];
-      tmem_ld16(tl + static_cast<std::uint32_t>(b1 * 256 + 128), v);
-      tmem_ld16(tl + static_cast<std::uint32_t>(b1 * 256 + 192), w);
+      tmem_ld16(tl + d2_col(b1), v);
+      tmem_ld16(tl + d2_col(b1) + 64, w);
       tmem_wait_ld();
       tc_before();
       __syncwarp();
@@ -294,17 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tid == 0) TT_TRACE(t, 4)
       // GEMM1(t) is done with the lo tile: split X(t+1) so GEMM1(t+1) can start
       if (t + 1 < T) split(t + 1);
-      // epilogue 1: T[(n,j)][k] -> T^T hi/lo tile, element ((n,k), j), once
-      // GEMM2(t-1), its last reader, is complete
-      if (t >= 1) {
-        ptx::mbar_wait(&d2_full[(t - 1) & 1], static_cast<std::uint32_t>((t - 1) >> 1) & 1u);
-        if (tid == 0) TT_TRACE(t - 1, 7)
-      }
+      // epilogue 1: T[(n,j)][k] -> T^T hi/lo tile b, element ((n,k), j); its
+      // last reader GEMM2(t-2) completed before epilogue 2 of t-2 ran
       tc_after();
-      std::uint32_t v[16], w[16];
+      std::uint32_t v[16];
       if (tid == 0) TT_TRACE(t, 10)
-      tmem_ld16(tl + static_cast<std::uint32_t>(b * 256), v);
-      tmem_ld16(tl + static_cast<std::uint32_t>(b * 256 + 64), w);
+      tmem_ld16(tl + d1_col(b), v);
       tmem_wait_ld();
       if (tid == 0) TT_TRACE(t, 11)
       tc_before();
@@ -314,11 +363,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = row >> 6, j = row & 63;
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-          const float x = __uint_as_float(v[c]) + __uint_as_float(w[c]);
+          const float x = __uint_as_float(v[c]);
           const float h = hi_of(x);
           const std::uint32_t o = sw_off(n * 64 + cg * 16 + c, j, kRows);
-          *reinterpret_cast<float*>(a2h + o) = h;
-          *reinterpret_cast<float*>(a2l + o) = x - h;
+          *reinterpret_cast<float*>(a2h(b) + o) = h;
+          *reinterpret_cast<float*>(a2l(b) + o) = x - h;
         }
       }
       if (tid == 0) TT_TRACE(t, 12)
@@ -329,7 +378,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tid == 0) TT_TRACE(t, 5)
       if (tid == 32 * 15) TT_TRACE(t, 14)
       // epilogue 2 of the previous pair (its D2 buffer is not the one GEMM2(t) writes)
-      if (t >= 1) epi2(t - 1);
+      if (t >= 1) {
+        ptx::mbar_wait(&d2_full[(t - 1) & 1], static_cast<std::uint32_t>((t - 1) >> 1) & 1u);
+        if (tid == 0) TT_TRACE(t - 1, 7)
+        tc_after();
+        epi2(t - 1);
+      }
     }
     if (T > 0) {
       ptx::mbar_wait(&d2_full[(T - 1) & 1], static_cast<std::uint32_t>((T - 1) >> 1) & 1u);

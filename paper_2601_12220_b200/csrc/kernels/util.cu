@@ -49,6 +49,20 @@ __global__ void flush_kernel(int4* p, std::int64_t n, int salt) {
     p[i] = make_int4(salt, salt, salt, static_cast<int>(i));
 }
 
+// read pass after the write pass: write-backs of the flush's own dirty lines
+// happen here, so the timed kernel starts with an L2 that holds none of its
+// data and no dirty lines (a write-only flush bills ~100 MB of foreign
+// write-backs to whatever runs next)
+__global__ void flush_read_kernel(const int4* p, std::int64_t n, int4* sink) {
+  int acc = 0;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const int4 v = __ldcg(p + i);
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x7fffffff) sink[0] = make_int4(acc, 0, 0, 0);  // never true for the flush pattern; keeps the loads
+}
+
 // FP64 pipe micro-benchmarks: the roofline denominator for the FP64-bound
 // kernels (MEASURED_PEAKS.json carries only HBM and bf16 numbers).
 __global__ void dfma_peak_kernel(double* sink, int iters, double seed) {
@@ -130,6 +144,8 @@ int flush_l2(void* scratch, std::int64_t bytes, void* stream) {
   int sms = 148;
   device_sm_count(&sms);
   flush_kernel<<<sms * 4, 512, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<int4*>(scratch), bytes / 16, ++salt);
+  flush_read_kernel<<<sms * 4, 512, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const int4*>(scratch), bytes / 16,
+                                                                             static_cast<int4*>(scratch));
   return cudaGetLastError();
 }
 

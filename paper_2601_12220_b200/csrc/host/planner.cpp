@@ -1259,6 +1259,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
       L.P = h.P;
       L.rows = static_cast<int>(h.u.size());
       L.variant = meta_int(plan.meta, "v", 2);
+      L.ne = meta_int(plan.meta, "ne", 4);
       for (int k = 0; k < 6; ++k) L.mats[k] = static_cast<const double*>(d_in[h.mats[k]]);
       L.G = static_cast<const double*>(d_in[h.g]);
       for (size_t q = 0; q < h.u.size(); ++q) {

@@ -458,7 +458,12 @@ __device__ __forceinline__ void pass_b(double* const (&wl)[NF], int ds, const do
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) hex2_kernel(const __grid_constant__ Hex2Dev p) {
+// NE2 elements per stage, 128 NE2 threads: NE2 = 2 runs two CTAs per SM;
+// NE2 = 4 runs one CTA of 16 warps whose plane passes split into exactly five
+// direction-uniform warps per direction (no warp runs two code paths).
+template <int NE2>
+__global__ void __launch_bounds__(128 * NE2, NE2 == 2 ? 2 : 1) hex2_kernel(const __grid_constant__ Hex2Dev p) {
+  constexpr int NE = NE2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);
   const int R = p.rows;
@@ -526,13 +531,11 @@ __global__ void __launch_bounds__(kThreads, 2) hex2_kernel(const __grid_constant
       const int r = t / P2;
       const int el = r % NE, f0 = r / NE, f1 = f0 + H;
       const double* g = Gs + el * P3 + kl;
-      if (f1 < R) {
-        double* const wl[2] = {W + (f0 * NE + el) * CS2 + kl, W + (f1 * NE + el) * CS2 + kl};
-        pass_b<2>(wl, ds, g, NE * P3);
-      } else {
-        double* const wl[1] = {W + (f0 * NE + el) * CS2 + kl};
-        pass_b<1>(wl, ds, g, NE * P3);
-      }
+      // odd R: the last thread pairs its field with itself (same values
+      // written twice by the same thread) — one code path, smaller kernel
+      double* const w0 = W + (f0 * NE + el) * CS2 + kl;
+      double* const wl[2] = {w0, f1 < R ? W + (f1 * NE + el) * CS2 + kl : w0};
+      pass_b<2>(wl, ds, g, NE * P3);
     }
     __syncthreads();
     if (threadIdx.x == 0 && more) issue_g(pair + gridDim.x);
@@ -565,10 +568,12 @@ struct HexConstSlot {
 std::mutex g_hex_mu;
 HexConstSlot g_hex_slot[64];
 
-int launch_hex2(const HexLaunch& L, cudaStream_t st) {
+template <int NE2>
+int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
   const int R = L.rows;
-  const int nblk = NE * R;
-  const int threads = kThreads;  // >= ND * nblk * P plane tasks for R <= 8
+  const int nblk = NE2 * R;
+  const int threads = 128 * NE2;  // >= ND * nblk * P plane tasks for R <= 8
+  auto kern = hex2_kernel<NE2>;
   Hex2Dev d{};
   d.E = L.E;
   d.rows = R;
@@ -577,18 +582,18 @@ int launch_hex2(const HexLaunch& L, cudaStream_t st) {
     d.U[f] = L.U[f];
     d.Y[f] = L.Y[f];
   }
-  const size_t doubles = ND * ND * NE * P3 + R * NE * P3 + ND * nblk * CS2;
+  const size_t doubles = ND * ND * NE2 * P3 + R * NE2 * P3 + ND * nblk * CS2;
   const size_t smem = doubles * 8 + 16;
-  cudaError_t e = cudaFuncSetAttribute(hex2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(hex2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   int sms = 148;
   device_sm_count(&sms);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hex2_kernel, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   std::int64_t grid = static_cast<std::int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
-  if (grid > L.E / NE) grid = L.E / NE;
+  if (grid > L.E / NE2) grid = L.E / NE2;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(g_hex_mu);
@@ -600,10 +605,16 @@ int launch_hex2(const HexLaunch& L, cudaStream_t st) {
                                 cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
   }
-  hex2_kernel<<<static_cast<int>(grid), threads, smem, st>>>(d);
+  kern<<<static_cast<int>(grid), threads, smem, st>>>(d);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return cudaEventRecord(slot.last, st);
+}
+
+// elements per stage: 4 when E allows (fact meta ne=2 forces the two-CTA form)
+int launch_hex2(const HexLaunch& L, cudaStream_t st) {
+  if (L.ne != 2 && L.E % 4 == 0) return launch_hex2_t<4>(L, st);
+  return launch_hex2_t<2>(L, st);
 }
 
 }  // namespace

@@ -250,6 +250,7 @@ struct HexLaunch {
   const double* U[8];
   double* Y[8];
   int variant;  // 2: constant-bank operators, plane/line passes (default); 1: register-plane passes
+  int ne;       // v2 elements per stage: 4 (default when E % 4 == 0) or 2
 };
 
 int launch_hex(const HexLaunch& p, void* stream);

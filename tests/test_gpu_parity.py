@@ -346,19 +346,26 @@ def test_tensor_train_f32_tensor_cores(fe, torch_cuda, n, meta):
     assert err <= max(1e-5, 4 * err_f32), (err, err_f32)
 
 
-@pytest.mark.parametrize("meta", ["", "v=1"])
+_HEX_WANT = {}
+
+
+@pytest.mark.parametrize("meta", ["", "ne=2", "v=1"])
 def test_hex_sumfact_small(fe, ref, torch_cuda, meta):
     """C2's sum-factorised operator at oracle-sized extents, both kernel
     variants, with shared (A_d) and six distinct forward/backward operators."""
     from paper_2601_12220_b200 import configs as C
-    for E, b, distinct in [(2, 1, False), (4, 3, False), (2, 8, True), (6, 5, True)]:
+    # E % 4 == 0 cases run the four-element stage, the others the two-element one
+    for E, b, distinct in [(2, 1, False), (4, 3, False), (2, 8, True), (6, 5, True), (4, 2, True), (8, 1, False)]:
         e = C.hex_poisson(E=E, b=b, distinct=distinct)
         opts = {"meta": meta, "transform": "hex_sumfact/v1"} if meta else None
         plan = fe.Plan(einsum=e, options=opts) if opts else fe.Plan(einsum=e)
         assert plan.info["transform"] == "hex_sumfact/v1"
         bind = ref.random_bindings(e, E + b)
         got = run_plan(torch_cuda, plan, bind)
-        want = ref.evaluate(e, bind)
+        key = (E, b, distinct)
+        if key not in _HEX_WANT:  # the oracle is slow here: evaluate once for all variants
+            _HEX_WANT[key] = ref.evaluate(e, bind)
+        want = _HEX_WANT[key]
         for g, w in zip(got, want):
             assert rel_err(g, w) <= FP64_TOL, (E, b)
 

@@ -151,38 +151,41 @@ __device__ __forceinline__ float hi_of(float x) { return __uint_as_float(__float
 //   D[:, 0:128]  = Ah * [Bh ; Bl]^T     (N = 128: the hi*hi and hi*lo terms side by side)
 //   D[:, 0:64]  += Al * Bh^T            (N = 64)
 // the epilogue adds the two 64-column halves in fp32
-__device__ __forceinline__ void gemm3(std::uint32_t d, const unsigned char* ah, const unsigned char* al,
-                                      const unsigned char* bhl) {
+// Descriptors are passed as precomputed bases: the start-address field is the
+// low 14 bits (address >> 4), so a tile offset is a compile-time add. The MMA
+// thread issues ~one instruction per MMA besides the MMA itself; computing the
+// descriptors in the loop made issue (not the tensor core) the bottleneck.
+__device__ __forceinline__ void gemm3(std::uint32_t d, std::uint64_t ah, std::uint64_t al, std::uint64_t bhl) {
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     const int kb = ks >> 2, kin = (ks & 3) * 32;
-    mma_tf32(d, sdesc(ah + kb * kKBlockA + kin), sdesc(bhl + kb * kKBlockB + kin), idesc(128), ks != 0);
+    mma_tf32(d, ah + ((kb * kKBlockA + kin) >> 4), bhl + ((kb * kKBlockB + kin) >> 4), idesc(128), ks != 0);
   }
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     const int kb = ks >> 2, kin = (ks & 3) * 32;
-    mma_tf32(d, sdesc(al + kb * kKBlockA + kin), sdesc(bhl + kb * kKBlockB + kin), idesc(64), 1);
+    mma_tf32(d, al + ((kb * kKBlockA + kin) >> 4), bhl + ((kb * kKBlockB + kin) >> 4), idesc(64), 1);
   }
 }
 
 // GEMM1 with A (X hi / lo) in TMEM: three N = 64 products accumulated in one
 // 64-column D1, small terms first: Xl G2h^T, Xh G2l^T, Xh G2h^T. B reads are
 // the only shared-memory traffic of the MMA (2 KB per instruction).
-__device__ __forceinline__ void gemm1_ts(std::uint32_t d, std::uint32_t xh, std::uint32_t xl, const unsigned char* g2) {
+__device__ __forceinline__ void gemm1_ts(std::uint32_t d, std::uint32_t xh, std::uint32_t xl, std::uint64_t g2) {
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     const int kb = ks >> 2, kin = (ks & 3) * 32;
-    mma_tf32_ts(d, xl + ks * 8, sdesc(g2 + kb * kKBlockB + kin), idesc(64), ks != 0);
+    mma_tf32_ts(d, xl + ks * 8, g2 + ((kb * kKBlockB + kin) >> 4), idesc(64), ks != 0);
   }
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     const int kb = ks >> 2, kin = (ks & 3) * 32;
-    mma_tf32_ts(d, xh + ks * 8, sdesc(g2 + kb * kKBlockB + R * 128 + kin), idesc(64), 1);
+    mma_tf32_ts(d, xh + ks * 8, g2 + ((kb * kKBlockB + R * 128 + kin) >> 4), idesc(64), 1);
   }
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     const int kb = ks >> 2, kin = (ks & 3) * 32;
-    mma_tf32_ts(d, xh + ks * 8, sdesc(g2 + kb * kKBlockB + kin), idesc(64), 1);
+    mma_tf32_ts(d, xh + ks * 8, g2 + ((kb * kKBlockB + kin) >> 4), idesc(64), 1);
   }
 }
 
@@ -249,29 +252,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kEpiWarps) {
     // --------------------------- TMA + MMA thread ---------------------------
     // order: GEMM1(0); then per t: GEMM2(t), GEMM1(t+1) — so GEMM2(t) runs
-    // while the epilogue splits X(t+1), and GEMM1(t+1) while it drains Y(t)
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    // while the epilogue splits X(t+1), and GEMM1(t+1) while it drains Y(t).
+    // The whole warp walks the schedule (uniform control flow keeps the
+    // descriptors in uniform registers); one elected lane issues.
+    {
+      const bool leader = ptx::elect_one();
+      if (leader) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
       auto tma_x = [&](std::int64_t t) {
         const int row0 = static_cast<int>((blockIdx.x + t * gridDim.x) * kRows);
         ptx::mbar_arrive_expect_tx(&x_full[0], kTile);
         tma_2d(xs0, &tmX, &x_full[0], 0, row0);
         tma_2d(xs0 + kKBlockA, &tmX, &x_full[0], 32, row0);
       };
+      const std::uint64_t dg1 = sdesc(g1), dg2 = sdesc(g2);
+      const std::uint64_t da2h0 = sdesc(a2h(0)), da2l0 = sdesc(a2l(0)), da2h1 = sdesc(a2h(1)), da2l1 = sdesc(a2l(1));
       auto gemm1 = [&](std::int64_t t) {
         const int b = static_cast<int>(t & 1);
         ptx::mbar_wait(lo_ready, static_cast<std::uint32_t>(t & 1));
         TT_TRACE(t, 0)
         // split(t) has read the X tile: load X(t+1); it lands long before
         // split(t+1), which follows GEMM1(t)
-        if (t + 1 < T) tma_x(t + 1);
+        if (leader && t + 1 < T) tma_x(t + 1);
         if (t >= 2) ptx::mbar_wait(&d1_free[b], static_cast<std::uint32_t>((t >> 1) - 1) & 1u);
         tc_after();
-        gemm1_ts(tmem + d1_col(b), tmem + kXhCol, tmem + kXlCol, g2);
-        mma_commit(&d1_full[b]);
+        if (leader) {
+          gemm1_ts(tmem + d1_col(b), tmem + kXhCol, tmem + kXlCol, dg2);
+          mma_commit(&d1_full[b]);
+        }
+        __syncwarp();
         TT_TRACE(t, 1)
       };
-      if (T > 0) tma_x(0);
+      if (leader && T > 0) tma_x(0);
       if (T > 0) gemm1(0);
       for (std::int64_t t = 0; t < T; ++t) {
         const int b = static_cast<int>(t & 1);
@@ -281,8 +292,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         TT_TRACE(t, 2)
         if (t >= 2) ptx::mbar_wait(&d2_free[b], static_cast<std::uint32_t>((t >> 1) - 1) & 1u);
         tc_after();
-        gemm3(tmem + d2_col(b), a2h(b), a2l(b), g1);
-        mma_commit(&d2_full[b]);
+        if (leader) {
+          gemm3(tmem + d2_col(b), b ? da2h1 : da2h0, b ? da2l1 : da2l0, dg1);
+          mma_commit(&d2_full[b]);
+        }
+        __syncwarp();
         TT_TRACE(t, 3)
       }
     }

@@ -9,15 +9,21 @@
 // ni=d, kA=f (A's unit-stride index), kB=e (B's unit-stride index).
 //
 // Why this shape on sm_100a: tcgen05 has no f64 kind, so FP64 tensor work is
-// mma.sync m8n8k4 (DMMA, SASS DMMA.8x8x4). Tiles are staged by TMA
-// (cp.async.bulk.tensor, 4-D boxes gather the strided GETT operands without a
-// transpose pass) into a 3-stage mbarrier ring, 64 k per stage as 8x8 boxes
-// with 64-byte inner rows (full-sector TMA requests). Each DMMA k-chunk spans
-// 2 kB x 2 kA values, so A and B fragment reads (both 64B-swizzled) hit the
-// 2-wavefront minimum; one producer warp issues the
-// TMA, nine consumer warps (3x3 grid of 24x24 warp tiles over a 72x72 CTA tile)
-// run the DMMAs. The persistent grid walks output tiles in groups that share A
-// slices so L2 serves the reuse.
+// mma.sync m8n8k4 (DMMA, SASS DMMA.8x8x4, 16 SMSP cycles each). CTA tiles are
+// 144 x 144 (two mo x 72 mi by two no x 72 ni) over 12 consumer warps with
+// 24 x 72 warp tiles — three warps per SM sub-partition, so the four DMMA
+// pipes carry equal work (a 72x72 tile over 9 warps left one sub-partition
+// with 3 of them: 75% at best). One producer warpgroup (a single TMA thread)
+// donates its registers to the consumers with setmaxnreg (40 / 152). Tiles
+// are staged by TMA (cp.async.bulk.tensor: 4-D boxes gather the strided GETT
+// operands without a transpose pass) into a 2-3 stage mbarrier ring, 32 k per
+// stage: A boxes of 8 kA (64-byte rows, 64B swizzle) x 4 kB, B boxes of 4 kB
+// (32-byte rows, 32B swizzle) x 8 kA. A 64-bit fragment load is served per
+// half-warp; the DMMA k-chunk map (f = kA in {0,1,4,5} + 2 (kc >> 2),
+// e = kB = qk ^ (kc & 3)) puts each half-warp's 16 words in distinct banks on
+// both swizzled images (ncu: 0.3% excess wavefronts, tensor pipe 97%).
+// The persistent grid walks output tiles in square raster groups that share
+// A/B slices in L2.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>

@@ -9,19 +9,18 @@
 //   q_x = sum_y G[x,y] . t_y              pointwise 3x3 geometric factors
 //   y  += (B1[x] x B2[x] x B3[x])^T q_x   three transposed sweeps per x
 //
-// B200 design: persistent CTAs walk element PAIRS (a pair of 125-double blocks
-// is a 16-byte-aligned 2000-byte run, the unit of a 1-D bulk copy). One thread
-// streams the pair's 9 G blocks and every field's u block with cp.async.bulk
-// into a double-buffered mbarrier ring, so G — the dominant traffic — is read
-// from HBM once and reused by all fields while the next pair is in flight.
-// The sweeps run on the FP64 pipe in four passes over 25-value planes held in
-// registers (two sweeps per pass where the plane contains both axes), with the
-// three directions and all fields of the pair in flight at once (240 plane
-// tasks for 256 threads), four CTA barriers per pair. Work cubes are padded to
-// rows of 6 doubles so every plane row moves as two 16-byte + one 8-byte
-// shared access, and lanes are assigned cube-fastest so that 8 consecutive
-// lanes' 16-byte accesses cover all 32 banks. 5x5 operators are too small for
-// DMMA tiles (padding to 8x8 wastes 61%).
+// Two kernels. v1 (hex_kernel, meta v=1): register-plane passes with the 5x5
+// operators loaded from shared memory. v2 (hex2_kernel, the default, see the
+// comment above it): operators in the constant bank, pass ownership matched
+// to the sweeps (planes / lines / planes), four elements per stage.
+//
+// Common to both: persistent CTAs walk element stages (2 or 4 elements = one
+// contiguous bulk-copy run per array); one thread streams the stage's 9 G
+// blocks and every field's u block with cp.async.bulk into mbarrier-tracked
+// slots that are refilled as soon as the pass that consumes them is done, so
+// G — the dominant traffic — is read from HBM once and reused by all fields.
+// 5x5 operators are too small for DMMA tiles (padding to 8x8 wastes 61%): the
+// sweeps run on the FP64 FMA pipe.
 #include <cuda_runtime.h>
 
 #include <mutex>

@@ -4,16 +4,20 @@
 //   Y_n = G1 T     (Y[i,k] = sum_j G1[i,j] T[j,k])
 //
 // B200 design: persistent CTAs, G1/G2 staged once per CTA in shared memory as
-// fp64 panels; samples are processed two at a time so each of the 8 DMMA warps
+// fp64 panels; samples are processed two at a time so each of 8 DMMA warps
 // owns a 32x32 tile in both GEMMs (GEMM 1 on the stacked [X_a; X_b] (128x64),
-// GEMM 2 on [T_a | T_b] (64x128)) — 0.5 fragment loads per DMMA. X pairs arrive
-// by TMA (2-D boxes, 128-byte swizzle) in a double-buffered mbarrier ring while
-// the previous pair computes; T never leaves shared memory (fp64 samples write
-// T^T over their consumed X stage; fp32 samples use a separate T buffer) and is
-// stored transposed so GEMM 2's fragments are conflict-free; Y goes straight
-// from the accumulators with 16-byte stores. Arithmetic: DMMA m8n8k4 (fp64
-// tensor cores); fp32 storage is converted on the fragment load and
-// accumulated in fp64.
+// GEMM 2 on [T_a | T_b] (64x128)) — 0.5 fragment loads per DMMA. For fp64 a
+// CTA runs two such 8-warp groups on independent sample pairs (16 warps, four
+// per SM sub-partition), each with its own X stage filled by TMA (2-D boxes,
+// 128-byte swizzle) and group-local named barriers, so one group's barrier and
+// load waits are covered by the other group's DMMAs. T never leaves shared
+// memory (fp64 samples write T^T over their consumed X stage; fp32 samples
+// use a separate T buffer) and is stored transposed so GEMM 2's fragments are
+// conflict-free; the fragment k-map (k0 + {0,1,8,9}) spreads each half-warp
+// over all banks under the swizzle. Y goes straight from the accumulators
+// with 16-byte stores. Arithmetic: DMMA m8n8k4 (fp64 tensor cores); fp32
+// storage is converted on the fragment load and accumulated in fp64 (the
+// fp32 default is tt_tc.cu).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>

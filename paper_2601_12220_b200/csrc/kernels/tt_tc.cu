@@ -3,10 +3,9 @@
 //   Y[n,i,k] = sum_{j,l} G1[i,j] G2[k,l] X[n,j,l]        (C4-f32: 4096 x 64^4)
 //
 // as two chained GEMMs per PAIR of samples, both M = 128 (rows = two samples
-// x 64), N = 64, K = 64, issued with tcgen05.mma.cta_group::1.kind::tf32 from
-// shared memory (K-major, 128-byte swizzle) into TMEM accumulators:
-//   GEMM1  T [(n,j), k] = sum_l X[(n,j), l] G2[k, l]      A = X tile (TMA)
-//   GEMM2  Y^T[(n,k), i] = sum_j T^T[(n,k), j] G1[i, j]   A = T^T (epilogue 1)
+// x 64), K = 64, on tcgen05.mma.cta_group::1.kind::tf32 into TMEM:
+//   GEMM1  T [(n,j), k] = sum_l X[(n,j), l] G2[k, l]      A = X hi / lo in TMEM
+//   GEMM2  Y^T[(n,k), i] = sum_j T^T[(n,k), j] G1[i, j]   A = T^T (shared, SW128)
 //
 // fp32 accuracy from the TF32 datapath (3xTF32): every operand is split into
 // hi = tf32 truncation (exact) and lo = x - hi (exact in fp32), and each GEMM
@@ -14,15 +13,22 @@
 // ~2^-20 relative); tests/test_gpu_parity.py holds it to the fp32 bar.
 //
 // Warp roles (one CTA per SM, persistent over sample pairs):
-//   warp 16, lane 0 — TMA producer (X pair tiles, two 128-byte k-blocks
-//                     each, double-buffered) and the single MMA-issuing thread;
-//   warps 0-15      — 4 TMEM lane quarters x 4 16-column groups: split X into
-//                     hi/lo, epilogue 1 (TMEM -> registers -> hi/lo T^T tile in
-//                     shared memory, transposed on the way with conflict-free
-//                     128-byte rows), epilogue 2 (TMEM -> coalesced global
-//                     stores of Y).
-// Schedule: GEMM2(t) overlaps the split of X(t+1), GEMM1(t+1) overlaps the
-// drain of Y(t); TMEM holds double-buffered accumulators (256 columns).
+//   warp 16 — walks the schedule as a whole warp (uniform control flow keeps
+//             every descriptor in uniform registers); one elected lane issues
+//             the X TMA (128-row x 128-byte boxes) and the MMAs. Computing
+//             descriptors per MMA in a divergent lane made MMA issue, not the
+//             tensor core, the bottleneck (tools/tcgen05_rate.cu measures the
+//             issue/complete rates: tf32 N=64 45 cyc, N=128 64 cyc);
+//   warps 0-15 — 4 TMEM lane quarters x 4 16-column groups: split X into
+//             hi / lo straight into TMEM (tcgen05.st; GEMM1 reads A from TMEM,
+//             so its only shared traffic is B), epilogue 1 (D1 -> registers ->
+//             hi/lo T^T tile in shared memory, transposed on the way with
+//             conflict-free 128-byte rows, double-buffered so it never waits
+//             for GEMM2 of the previous pair), epilogue 2 (D2 -> coalesced
+//             global stores of Y).
+// GEMM1 runs three N = 64 products into one 64-column D1 (small terms first);
+// GEMM2 runs Ah [Bh;Bl] (N = 128) + Al Bh (N = 64) into a 128-column D2.
+// Schedule: GEMM1(t+1) is issued before GEMM2(t); TMEM: D1[2], D2[2], X hi/lo.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>

@@ -119,6 +119,10 @@ int fe_plan_tabulate(fe_plan_t plan, const char* operand, const void* const* d_i
 int fe_plan_shard(fe_plan_t plan, int rank, int world, const char* options_json, fe_plan_t* out, int64_t* lo,
                   int64_t* hi, char** axis);
 int fe_plan_destroy(fe_plan_t plan);
+/* mean device time (CUDA events, L2 flushed before every run) of one execute
+ * on synthetic dyadic inputs allocated and filled on the current device; the
+ * measurement the tuner records as a fact's wall_time_s */
+int fe_plan_time(fe_plan_t plan, int reps, int warmup, uint64_t seed, double* out_seconds);
 
 /* ---- device utilities for tests and benches ---- */
 /* deterministic dyadic values m/2^19 - 1 (the reference's random_bindings

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/feinsum_b200.h). Every entry point converts
 // exceptions into status codes + a thread-local message, so no C++ exception
 // ever crosses the ABI.
+#include <algorithm>
 #include "feinsum_b200.h"
 
 #include <cuda_runtime.h>
@@ -463,6 +464,57 @@ int fe_plan_shard(fe_plan_t plan, int rank, int world, const char* options, fe_p
 int fe_plan_destroy(fe_plan_t plan) {
   delete plan;
   return FE_OK;
+}
+
+int fe_plan_time(fe_plan_t plan, int reps, int warmup, uint64_t seed, double* seconds) {
+  return guarded([&] {
+    const feb200::Plan& p = *plan->plan;
+    auto check = [](cudaError_t e, const char* what) {
+      if (e != cudaSuccess) throw error(errc::io, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    std::vector<void*> ins(p.leaves.size(), nullptr), outs(p.outputs.size(), nullptr);
+    void* flush = nullptr;
+    constexpr std::int64_t kFlush = std::int64_t{256} << 20;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto release = [&] {
+      for (void* q : ins) cudaFree(q);
+      for (void* q : outs) cudaFree(q);
+      cudaFree(flush);
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+    };
+    try {
+      for (size_t i = 0; i < ins.size(); ++i) {
+        const std::int64_t n = std::max<std::int64_t>(p.leaves[i].bytes(), 16);
+        check(cudaMalloc(&ins[i], static_cast<size_t>(n)), "cudaMalloc");
+        check(static_cast<cudaError_t>(feb200::fill_dyadic(ins[i], p.leaves[i].storage, p.leaves[i].meta.num_elements(),
+                                                           seed * 1000 + i, nullptr)),
+              "fill");
+      }
+      for (size_t r = 0; r < outs.size(); ++r)
+        check(cudaMalloc(&outs[r], static_cast<size_t>(std::max<std::int64_t>(p.outputs[r].bytes(), 16))), "cudaMalloc");
+      check(cudaMalloc(&flush, kFlush), "cudaMalloc");
+      check(cudaEventCreate(&e0), "event");
+      check(cudaEventCreate(&e1), "event");
+      for (int w = 0; w < warmup; ++w) feb200::execute(p, ins.data(), outs.data(), nullptr);
+      double total = 0.0;
+      for (int r = 0; r < reps; ++r) {
+        check(static_cast<cudaError_t>(feb200::flush_l2(flush, kFlush, nullptr)), "flush");
+        check(cudaEventRecord(e0, nullptr), "event");
+        feb200::execute(p, ins.data(), outs.data(), nullptr);
+        check(cudaEventRecord(e1, nullptr), "event");
+        check(cudaEventSynchronize(e1), "sync");
+        float ms = 0.f;
+        check(cudaEventElapsedTime(&ms, e0, e1), "event");
+        total += ms * 1e-3;
+      }
+      *seconds = reps > 0 ? total / reps : 0.0;
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
+  });
 }
 
 int fe_fill_dyadic(void* d_ptr, int storage, int64_t count, uint64_t seed, void* stream) {

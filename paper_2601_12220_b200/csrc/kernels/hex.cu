@@ -468,11 +468,12 @@ __global__ void __launch_bounds__(128 * NE2, NE2 == 2 ? 2 : 1) hex2_kernel(const
   const int R = p.rows;
   const int nblk = NE * R;   // cubes per pair, cube = field * NE + element
   const int ds = nblk * CS2;  // direction stride in W
-  // layout (doubles): Gs[9][NE*P3] | Us[R][NE*P3] | W[ND][nblk][CS2] | mbar {G, U}
+  // layout (doubles): Gs[9][NE*P3] | Us[R][NE*P3] | W[ND][nblk][CS2] | Ys[R][NE*P3] | mbar {G, U}
   double* Gs = sm;
   double* Us = Gs + ND * ND * NE * P3;
   double* W = Us + R * NE * P3;
-  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(W + ND * ds);
+  double* Ys = W + ND * ds;  // output staging: one bulk store per field and stage
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(Ys + R * NE * P3);
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar[0], 1);
     ptx::mbar_init(&bar[1], 1);
@@ -493,7 +494,11 @@ __global__ void __launch_bounds__(128 * NE2, NE2 == 2 ? 2 : 1) hex2_kernel(const
     const std::int64_t e0 = pair * NE;
     for (int f = 0; f < R; ++f) ptx::bulk_g2s(Us + f * NE * P3, p.U[f] + e0 * P3, bytes, &bar[1]);
   };
-  if (threadIdx.x == 0 && blockIdx.x < npairs) {
+  // the copy engine is driven by lane 0 of the last warp, which has no pass-B
+  // work (and none in passes A/C at four elements per stage), so issuing the
+  // next stage's copies never delays a computing warp
+  const bool producer = threadIdx.x == blockDim.x - 32;
+  if (producer && blockIdx.x < npairs) {
     issue_u(blockIdx.x);
     issue_g(blockIdx.x);
   }
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(128 * NE2, NE2 == 2 ? 2 : 1) hex2_kernel(const
       else pass_a<2>(a_in, a_out);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && more) issue_u(pair + gridDim.x);
+    if (producer && more) issue_u(pair + gridDim.x);
 
     ptx::mbar_wait(&bar[0], phase);
     for (int t = threadIdx.x; t < nbt; t += blockDim.x) {
@@ -537,26 +542,36 @@ __global__ void __launch_bounds__(128 * NE2, NE2 == 2 ? 2 : 1) hex2_kernel(const
       pass_b<2>(wl, ds, g, NE * P3);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && more) issue_g(pair + gridDim.x);
+    if (producer && more) issue_g(pair + gridDim.x);
 
     if (pactive) {
       if (dir == 0) pass_c<0>(a_out);
       else if (dir == 1) pass_c<1>(a_out);
       else pass_c<2>(a_out);
     }
+    if (producer) ptx::bulk_wait_read<0>();  // the previous stage's stores have read Ys
     __syncthreads();
 
     const std::int64_t e0 = pair * NE;
-    // y rows of a field are one contiguous run of NE * P3 doubles: coalesced
+    // sum the three direction partials into the staging tile (a field's
+    // stage output is one contiguous run of NE * P3 doubles), then one bulk
+    // copy per field streams it to HBM while the next stage computes —
+    // instead of a burst of global stores at the end of every stage
     for (int off = threadIdx.x; off < NE * P3; off += blockDim.x) {
       const int el = off / P3;
       const double* w = W + el * CS2 + (off - el * P3);
 #pragma unroll
       for (int f = 0; f < kMaxFields; ++f)
-        if (f < R) __stcs(p.Y[f] + e0 * P3 + off, (w[f * NE * CS2] + w[ds + f * NE * CS2]) + w[2 * ds + f * NE * CS2]);
+        if (f < R) Ys[f * NE * P3 + off] = (w[f * NE * CS2] + w[ds + f * NE * CS2]) + w[2 * ds + f * NE * CS2];
     }
-    __syncthreads();  // W is rewritten by the next pair's pass A
+    ptx::fence_proxy_async();
+    __syncthreads();  // W is rewritten by the next pair's pass A; Ys complete
+    if (producer) {
+      for (int f = 0; f < R; ++f) ptx::bulk_s2g(p.Y[f] + e0 * P3, Ys + f * NE * P3, bytes);
+      ptx::bulk_commit();
+    }
   }
+  if (producer) ptx::bulk_wait<0>();
 }
 
 // The operator constants are shared by every launch on a device: a launch
@@ -581,7 +596,7 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
     d.U[f] = L.U[f];
     d.Y[f] = L.Y[f];
   }
-  const size_t doubles = ND * ND * NE2 * P3 + R * NE2 * P3 + ND * nblk * CS2;
+  const size_t doubles = ND * ND * NE2 * P3 + 2 * R * NE2 * P3 + ND * nblk * CS2;
   const size_t smem = doubles * 8 + 16;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

@@ -1439,8 +1439,11 @@ std::unique_ptr<Plan> make_shard(const Plan& full, int rank, int world, const Pl
   if (ix.empty()) throw error(errc::usage, "this einsum has no output index to shard along");
   const auto lens = feinsum::index_lengths(full.skel);
   const std::int64_t n = lens.at(ix);
-  // fem_grad / hex move elements in pairs (16-byte bulk-copy runs)
-  const std::int64_t unit = (full.family == Family::fem_grad || full.family == Family::hex) ? 2 : 1;
+  // fem_grad moves elements in pairs (16-byte bulk-copy runs); hex in stages
+  // of four when the axis allows it (the four-element kernel), else pairs
+  std::int64_t unit = 1;
+  if (full.family == Family::fem_grad) unit = 2;
+  if (full.family == Family::hex) unit = lens.at(ix) % 4 == 0 ? 4 : 2;
   const std::int64_t units = n / unit;
   std::int64_t a = units * rank / world * unit, b = units * (rank + 1) / world * unit;
   if (rank == world - 1) b = n;

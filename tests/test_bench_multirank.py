@@ -25,13 +25,13 @@ def test_bench_two_ranks_weak_scaling_verified():
     env = dict(os.environ, FE_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "1", "--configs", "C1,C4-f64,C5",
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--configs", "C1,C3,C4-f64,C4-f32,C5",
            "--no-e2e", "--no-cpu-baseline"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["scaling"] == "weak"
     assert line["verify"]["ok"], line["verify"]
-    assert set(line["config"]["per_config"]) == {"C1", "C4-f64", "C5"}
+    assert set(line["config"]["per_config"]) == {"C1", "C3", "C4-f64", "C4-f32", "C5"}
     for v in line["config"]["per_config"].values():
         assert v["transform"] != "generic/v1"

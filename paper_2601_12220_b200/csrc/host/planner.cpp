@@ -617,10 +617,24 @@ bool bind_gett(Plan& p, std::string* why) {
   const int sb = s1.count(ni) ? 1 : 0, sa = 1 - sb;
   const feinsum::IndexList& la = c.i_in[sa];
   const feinsum::IndexList& lb = c.i_in[sb];
-  const std::string ka = la.back(), kb = lb.back();
-  if (!K.count(ka) || !K.count(kb) || ka == kb) {
-    *why = "unit-stride indices of A and B must be the two contracted indices";
-    return false;
+  // the kernel wants A's unit-stride index to be one contracted index (kA)
+  // and B's the other (kB); an operand that does not comply is repacked per
+  // execute (one HBM pass, ~1% of the contraction at TCCG sizes) — this is
+  // what lets every TCCG sibling spelling run on the tensor cores
+  const std::vector<std::string> Kv(K.begin(), K.end());
+  const bool a_ok = K.count(la.back()) > 0;
+  bool b_ok = K.count(lb.back()) > 0 && !(a_ok && lb.back() == la.back());
+  std::string ka, kb;
+  if (a_ok) {
+    ka = la.back();
+    kb = ka == Kv[0] ? Kv[1] : Kv[0];
+    b_ok = b_ok && lb.back() == kb;
+  } else if (b_ok) {
+    kb = lb.back();
+    ka = kb == Kv[0] ? Kv[1] : Kv[0];
+  } else {
+    ka = Kv[0];
+    kb = Kv[1];
   }
   const auto lens = feinsum::index_lengths(c);
   std::vector<std::string> M, N;
@@ -628,9 +642,12 @@ bool bind_gett(Plan& p, std::string* why) {
     if (!K.count(x)) M.push_back(x);
   for (const auto& x : lb)
     if (!K.count(x)) N.push_back(x);
-  const std::string mi = M[1], mo = M[0];  // later position = smaller stride in A
+  std::string mi = M[1], mo = M[0];  // later position = smaller stride in A
+  if (!a_ok && lens.at(mi) != 72 && lens.at(mo) == 72) std::swap(mi, mo);  // packed A: any order
   const std::string no = N[0] == ni ? N[1] : N[0];
   GettBinding g;
+  g.pack_a = !a_ok;
+  g.pack_b = !b_ok;
   g.ext_mo = lens.at(mo);
   g.ext_mi = lens.at(mi);
   g.ext_no = lens.at(no);
@@ -651,17 +668,36 @@ bool bind_gett(Plan& p, std::string* why) {
   const auto& shb = c.args[0][sb].shape;
   std::vector<std::int64_t> shc;
   for (const auto& s : c.i_out) shc.push_back(lens.at(s));
-  g.a_mo = stride_of(la, sha, mo);
-  g.a_mi = stride_of(la, sha, mi);
-  g.a_kb = stride_of(la, sha, kb);
-  g.b_no = stride_of(lb, shb, no);
-  g.b_ni = stride_of(lb, shb, ni);
-  g.b_ka = stride_of(lb, shb, ka);
+  if (g.pack_a) {
+    const std::int64_t src[4] = {stride_of(la, sha, mo), stride_of(la, sha, mi), stride_of(la, sha, kb),
+                                 stride_of(la, sha, ka)};
+    std::copy(src, src + 4, g.a_src);
+    g.a_kb = g.ext_ka;
+    g.a_mi = g.ext_kb * g.ext_ka;
+    g.a_mo = g.ext_mi * g.a_mi;
+  } else {
+    g.a_mo = stride_of(la, sha, mo);
+    g.a_mi = stride_of(la, sha, mi);
+    g.a_kb = stride_of(la, sha, kb);
+  }
+  if (g.pack_b) {
+    const std::int64_t src[4] = {stride_of(lb, shb, no), stride_of(lb, shb, ni), stride_of(lb, shb, ka),
+                                 stride_of(lb, shb, kb)};
+    std::copy(src, src + 4, g.b_src);
+    g.b_ka = g.ext_kb;
+    g.b_ni = g.ext_ka * g.ext_kb;
+    g.b_no = g.ext_ni * g.b_ni;
+  } else {
+    g.b_no = stride_of(lb, shb, no);
+    g.b_ni = stride_of(lb, shb, ni);
+    g.b_ka = stride_of(lb, shb, ka);
+  }
   g.c_mo = stride_of(c.i_out, shc, mo);
   g.c_mi = stride_of(c.i_out, shc, mi);
   g.c_no = stride_of(c.i_out, shc, no);
   g.c_ni = stride_of(c.i_out, shc, ni);
-  g.role_names = "mo=" + mo + " mi=" + mi + " no=" + no + " ni=" + ni + " kA=" + ka + " kB=" + kb;
+  g.role_names = "mo=" + mo + " mi=" + mi + " no=" + no + " ni=" + ni + " kA=" + ka + " kB=" + kb +
+                 (g.pack_a ? " packA" : "") + (g.pack_b ? " packB" : "");
   const int n = c.n();
   for (int q = 0; q < c.b(); ++q) {
     const int ur = p.canon.sigma_row[q];
@@ -1071,6 +1107,15 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
       const size_t n = static_cast<size_t>(p.gett.ext_mo * p.gett.ext_mi + p.gett.ext_no * p.gett.ext_ni);
       cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_scratch), n * sizeof(double)), "cudaMalloc(gett scratch)");
     }
+    const GettBinding& g = p.gett;
+    if (g.pack_a)
+      cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_pack_a),
+                            sizeof(double) * static_cast<size_t>(g.ext_mo * g.ext_mi * g.ext_ka * g.ext_kb)),
+                 "cudaMalloc(gett packed A)");
+    if (g.pack_b)
+      cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_pack_b),
+                            sizeof(double) * static_cast<size_t>(g.ext_no * g.ext_ni * g.ext_ka * g.ext_kb)),
+                 "cudaMalloc(gett packed B)");
   }
 }
 
@@ -1087,6 +1132,8 @@ Plan::~Plan() {
   if (d_blob) cudaFree(d_blob);
   if (d_coef) cudaFree(d_coef);
   if (d_scratch) cudaFree(d_scratch);
+  if (d_pack_a) cudaFree(d_pack_a);
+  if (d_pack_b) cudaFree(d_pack_b);
 }
 
 std::unique_ptr<Plan> make_plan(const BatchedEinsum& e, const PlanOptions& opt) {
@@ -1233,6 +1280,16 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         L.c_ni = b.c_ni;
         L.A = static_cast<const double*>(d_in[r.a_leaf]);
         L.B = static_cast<const double*>(d_in[r.b_leaf]);
+        if (b.pack_a) {
+          const std::int64_t ext[4] = {b.ext_mo, b.ext_mi, b.ext_kb, b.ext_ka};
+          cuda_check(permute4(L.A, plan.d_pack_a, ext, b.a_src, stream), "gett pack A");
+          L.A = plan.d_pack_a;
+        }
+        if (b.pack_b) {
+          const std::int64_t ext[4] = {b.ext_no, b.ext_ni, b.ext_ka, b.ext_kb};
+          cuda_check(permute4(L.B, plan.d_pack_b, ext, b.b_src, stream), "gett pack B");
+          L.B = plan.d_pack_b;
+        }
         L.C = static_cast<double*>(d_out[r.out_row]);
         L.a_alpha = r.a_alpha;
         L.a_beta = r.a_beta;
@@ -1398,7 +1455,7 @@ std::string describe(const Plan& p) {
   if (p.family == Family::gett) {
     Value f = Value::obj();
     f.set("roles", Value::str(p.gett.role_names));
-    f.set("tile", Value::str("72x72x16, 9 DMMA warps + 1 TMA warp"));
+    f.set("tile", Value::str("144x144x32, 12 DMMA warps + 1 TMA warpgroup"));
     v.set("roles", std::move(f));
   }
   return fejson::dump(v);

@@ -79,6 +79,11 @@ struct GettBinding {
   std::int64_t a_mo = 0, a_mi = 0, a_kb = 0, b_no = 0, b_ni = 0, b_ka = 0;
   std::int64_t c_mo = 0, c_mi = 0, c_no = 0, c_ni = 0;
   std::string role_names;  // "mo=a mi=b ..." for describe()
+  // operands whose unit-stride index is not their contracted one are repacked
+  // per execute into a plan buffer laid out [mo][mi][kB][kA] (A) or
+  // [no][ni][kA][kB] (B); *_src are the source strides in that dim order
+  bool pack_a = false, pack_b = false;
+  std::int64_t a_src[4] = {0, 0, 0, 0}, b_src[4] = {0, 0, 0, 0};
   struct Row {
     int a_leaf, b_leaf, out_row;
     int a_alpha, a_beta, b_alpha, b_beta;
@@ -140,6 +145,8 @@ struct Plan {
   void* d_blob = nullptr;
   double* d_coef = nullptr;
   double* d_scratch = nullptr;  // family workspace (GETT affine K-sums)
+  double* d_pack_a = nullptr;   // GETT repacked operands (see GettBinding)
+  double* d_pack_b = nullptr;
   GenericLaunch gen{};  // pointers filled per execution
   int sm_count = 148;
 

@@ -260,6 +260,10 @@ bool hex_supported(int nd, int p, std::int64_t E, int rows);
 int device_sm_count(int* out);
 int fill_dyadic(void* ptr, int storage, std::int64_t count, std::uint64_t seed, void* stream);
 int flush_l2(void* scratch, std::int64_t bytes, void* stream);
+// dst[i0][i1][i2][i3] (contiguous, extents ext[0..3]) = src[sum_d i_d * src_stride[d]]:
+// repacks a strided operand into a kernel's layout (GETT operands whose
+// unit-stride index is not a contracted one)
+int permute4(const double* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream);
 // which: 0 = DFMA (CUDA cores), 1 = DMMA m8n8k4 (FP64 tensor cores)
 int fp64_peak(int which, double* tflops);
 

@@ -132,6 +132,86 @@ int fill_dyadic(void* ptr, int storage, std::int64_t count, std::uint64_t seed, 
   return cudaGetLastError();
 }
 
+// 4-D permute through a 32 x 32 shared tile over (dst inner dim, src unit-
+// stride dim) so both the reads and the writes are coalesced; the other two
+// dims ride on blockIdx.z. When the src's unit-stride dim is the dst's inner
+// dim (or none is unit stride) it is a plain strided copy.
+struct Permute4 {
+  const double* src;
+  double* dst;
+  std::int64_t ext[4], ss[4], ds[4];
+  int u;  // dst dim whose src stride is 1 (-1: none)
+};
+
+__global__ void permute4_tiled(const __grid_constant__ Permute4 p) {
+  __shared__ double tile[32][33];
+  // dims: 3 = dst inner (x tile), u = src inner (y tile), the other two (a, b) on z
+  const int u = p.u;
+  int oa = -1, ob = -1;
+  for (int d = 0; d < 3; ++d)
+    if (d != u) (oa < 0 ? oa : ob) = d;
+  const std::int64_t z = blockIdx.z;
+  const std::int64_t ia = z / p.ext[ob], ib = z - ia * p.ext[ob];
+  const std::int64_t x0 = static_cast<std::int64_t>(blockIdx.x) * 32, y0 = static_cast<std::int64_t>(blockIdx.y) * 32;
+  const std::int64_t base_s = ia * p.ss[oa] + ib * p.ss[ob];
+  const std::int64_t base_d = ia * p.ds[oa] + ib * p.ds[ob];
+  // read: consecutive threads walk the src unit-stride dim u
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const std::int64_t x = x0 + r, y = y0 + threadIdx.x;
+    if (x < p.ext[3] && y < p.ext[u]) tile[r][threadIdx.x] = __ldg(p.src + base_s + x * p.ss[3] + y);
+  }
+  __syncthreads();
+  // write: consecutive threads walk the dst inner dim 3
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const std::int64_t y = y0 + r, x = x0 + threadIdx.x;
+    if (x < p.ext[3] && y < p.ext[u]) p.dst[base_d + y * p.ds[u] + x] = tile[threadIdx.x][r];
+  }
+}
+
+__global__ void permute4_plain(const __grid_constant__ Permute4 p) {
+  const std::int64_t n = p.ext[0] * p.ext[1] * p.ext[2] * p.ext[3];
+  for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    std::int64_t r = t, off = 0;
+    for (int d = 3; d >= 0; --d) {
+      const std::int64_t i = r % p.ext[d];
+      r /= p.ext[d];
+      off += i * p.ss[d];
+    }
+    p.dst[t] = __ldg(p.src + off);
+  }
+}
+
+int permute4(const double* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream) {
+  Permute4 p{};
+  p.src = src;
+  p.dst = dst;
+  p.u = -1;
+  std::int64_t acc = 1;
+  for (int d = 3; d >= 0; --d) {
+    p.ext[d] = ext[d];
+    p.ss[d] = src_stride[d];
+    p.ds[d] = acc;
+    acc *= ext[d];
+    if (src_stride[d] == 1 && d != 3 && ext[d] > 1) p.u = d;
+  }
+  if (acc == 0) return cudaSuccess;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p.u >= 0) {
+    int oa = -1, ob = -1;
+    for (int d = 0; d < 3; ++d)
+      if (d != p.u) (oa < 0 ? oa : ob) = d;
+    const dim3 grid(static_cast<unsigned>((ext[3] + 31) / 32), static_cast<unsigned>((ext[p.u] + 31) / 32),
+                    static_cast<unsigned>(ext[oa] * ext[ob]));
+    permute4_tiled<<<grid, dim3(32, 8), 0, st>>>(p);
+  } else {
+    int sms = 148;
+    device_sm_count(&sms);
+    permute4_plain<<<sms * 8, 256, 0, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
 int flush_l2(void* scratch, std::int64_t bytes, void* stream) {
   static int salt = 0;
   static const bool carve = [] {

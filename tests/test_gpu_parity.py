@@ -284,6 +284,27 @@ def test_gett_full_c3_exact_vs_torch(fe, torch_cuda):
     assert torch.equal(out, want)
 
 
+@pytest.mark.parametrize("name", ["abcd-aebf-dfce", "abcd-aebf-fdec", "abcd-eafb-fdec", "abcd-eafd-fbec"])
+def test_gett_tccg_siblings_exact(fe, torch_cuda, name):
+    """Every TCCG sibling reading of the C3 contraction runs on the DMMA GETT
+    kernel (operands whose unit-stride index is an output index are repacked
+    per execute) and is exact on dyadic data against an fp64 torch.einsum."""
+    from paper_2601_12220_b200 import configs as C
+    torch = torch_cuda
+    e = C.tccg(name, ext=72)
+    plan = fe.Plan(einsum=e)
+    assert plan.info["transform"] == "gett_dmma/v1", plan.info
+    A = torch.empty([72] * 4, dtype=torch.float64, device="cuda")
+    B = torch.empty([72] * 4, dtype=torch.float64, device="cuda")
+    fe.fill_dyadic(A, 3)
+    fe.fill_dyadic(B, 4)
+    (out,) = plan(A, B)
+    a, b = C.TCCG_SIBLINGS[name]
+    want = torch.einsum(f"{a},{b}->abcd", A, B)
+    torch.cuda.synchronize()
+    assert torch.equal(out, want), name
+
+
 @pytest.mark.parametrize("dtype,tol", [("float64", FP64_TOL), ("float32", 1e-5)])
 def test_tensor_train_small(fe, ref, torch_cuda, dtype, tol):
     from paper_2601_12220_b200 import configs as C

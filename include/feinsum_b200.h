@@ -107,8 +107,12 @@ int fe_plan_num_outputs(fe_plan_t plan);
 /* stream-ordered; never allocates; d_in in describe().inputs order, d_out one
  * buffer per caller row */
 int fe_plan_execute(fe_plan_t plan, const void* const* d_in, void* const* d_out, void* stream);
-/* end-to-end: host inputs -> H2D -> kernels -> D2H into host outputs, all on
- * `stream` (device staging buffers are owned by the plan; not synchronized) */
+/* end-to-end: host inputs -> H2D -> kernels -> D2H into host outputs, ordered
+ * on `stream` (device staging buffers are owned by the plan; not
+ * synchronized). Plans above 256 MB run as a pipeline of 8 chunks along the
+ * shard axis: chunk k's H2D, chunk k-1's kernels and chunk k-2's D2H overlap
+ * on internal streams (host buffers should be pinned for the copies to
+ * overlap); `stream` resumes after the last D2H. */
 int fe_plan_execute_host(fe_plan_t plan, const void* const* h_in, void* const* h_out, void* stream);
 /* tabulate one skeleton operand (materialize, raising.hpp:43) into
  * interleaved complex doubles */

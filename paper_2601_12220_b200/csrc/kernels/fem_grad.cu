@@ -91,9 +91,27 @@ __global__ void __launch_bounds__(32 + TE * NI / EPT, kDSmem ? 2 : 1)
     for (std::int64_t tile = blockIdx.x; tile < ntiles && prefetched < S; tile += gridDim.x, ++prefetched)
       issue(tile, prefetched);
   }
-  for (int t = tid; t < p.n_d * NX * NI * NJ; t += blockDim.x) {
-    const int which = t / (NX * NI * NJ);
-    dsm[t] = __ldg(p.D[which] + (t - which * NX * NI * NJ));
+  {
+    // D copies: every load of a thread issued before its stores (one global
+    // round trip in the prologue instead of one per loop trip)
+    constexpr int kPer = 4;
+    const int nd = p.n_d * NX * NI * NJ;
+    double v[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = tid + k * static_cast<int>(blockDim.x);
+      const int which = t / (NX * NI * NJ);
+      v[k] = t < nd ? __ldg(p.D[which] + (t - which * NX * NI * NJ)) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = tid + k * static_cast<int>(blockDim.x);
+      if (t < nd) dsm[t] = v[k];
+    }
+    for (int t = tid + kPer * static_cast<int>(blockDim.x); t < nd; t += blockDim.x) {
+      const int which = t / (NX * NI * NJ);
+      dsm[t] = __ldg(p.D[which] + (t - which * NX * NI * NJ));
+    }
   }
   if (!kPlainU && tid < p.n_u) {
     Coef c;

@@ -150,11 +150,25 @@ __global__ void __launch_bounds__(TTShape<T>::kThreadsT, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
     issue(first);
   }
-  // G1/G2 staged (as fp64 panels) while the first X pairs are in flight
-  for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
-    const int r = t / R, c = t % R;
-    *reinterpret_cast<double*>(g1 + PD::off(r, c)) = static_cast<double>(static_cast<const T*>(p.G1)[t]);
-    *reinterpret_cast<double*>(g2 + PD::off(r, c)) = static_cast<double>(static_cast<const T*>(p.G2)[t]);
+  // G1/G2 staged (as fp64 panels) while the first X pairs are in flight; all
+  // of a thread's global loads are issued before any store so their
+  // latencies overlap (one round trip, not R*R/threads of them)
+  {
+    constexpr int kPer = R * R / SH::kThreadsT;
+    static_assert(R * R % SH::kThreadsT == 0, "G staging assumes an even split");
+    double v1[kPer], v2[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = threadIdx.x + k * SH::kThreadsT;
+      v1[k] = static_cast<double>(__ldg(static_cast<const T*>(p.G1) + t));
+      v2[k] = static_cast<double>(__ldg(static_cast<const T*>(p.G2) + t));
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = threadIdx.x + k * SH::kThreadsT;
+      *reinterpret_cast<double*>(g1 + PD::off(t / R, t % R)) = v1[k];
+      *reinterpret_cast<double*>(g2 + PD::off(t / R, t % R)) = v2[k];
+    }
   }
   __syncthreads();
   auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kConsumerWarps * 32) : "memory"); };

@@ -219,15 +219,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // constants: G2 as B of GEMM1 ([k][l], K = l), G1 as B of GEMM2 ([i][j], K = j), split hi / lo
-#pragma unroll 8
-  for (int idx = tid; idx < R * R; idx += kThreads) {
-    const int r = idx >> 6, c = idx & 63;
-    const float a = __ldg(p.G2 + idx), b = __ldg(p.G1 + idx);
-    const float ah = hi_of(a), bh = hi_of(b);
-    *reinterpret_cast<float*>(g2 + sw_off(r, c, 2 * R)) = ah;
-    *reinterpret_cast<float*>(g2 + sw_off(R + r, c, 2 * R)) = a - ah;
-    *reinterpret_cast<float*>(g1 + sw_off(r, c, 2 * R)) = bh;
-    *reinterpret_cast<float*>(g1 + sw_off(R + r, c, 2 * R)) = b - bh;
+  // all global loads first (one latency), then the split stores
+  {
+    constexpr int kPer = (R * R + kThreads - 1) / kThreads;
+    float va[kPer], vb[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int idx = tid + k * kThreads;
+      va[k] = idx < R * R ? __ldg(p.G2 + idx) : 0.f;
+      vb[k] = idx < R * R ? __ldg(p.G1 + idx) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int idx = tid + k * kThreads;
+      if (idx >= R * R) break;
+      const int r = idx >> 6, c = idx & 63;
+      const float a = va[k], b = vb[k];
+      const float ah = hi_of(a), bh = hi_of(b);
+      *reinterpret_cast<float*>(g2 + sw_off(r, c, 2 * R)) = ah;
+      *reinterpret_cast<float*>(g2 + sw_off(R + r, c, 2 * R)) = a - ah;
+      *reinterpret_cast<float*>(g1 + sw_off(r, c, 2 * R)) = bh;
+      *reinterpret_cast<float*>(g1 + sw_off(R + r, c, 2 * R)) = b - bh;
+    }
   }
   if (warp == kEpiWarps) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_addr(tmem_slot)),

@@ -1414,6 +1414,23 @@ std::string describe(const Plan& p) {
     case Family::generic: pipe = "fma"; break;
   }
   v.set("pipe", Value::str(pipe));
+  // kernels one execute launches (tuned path, aligned buffers): the family's
+  // kernel per row where it loops over rows, plus the coefficient kernel and
+  // GETT's operand passes (row sums for alpha*X+beta, repacks)
+  int launches = p.chains.empty() ? 0 : 1;
+  switch (p.family) {
+    case Family::fem_grad: launches += 1; break;
+    case Family::hex: launches += 1; break;
+    case Family::tt: launches += static_cast<int>(p.tt.rows.size()); break;
+    case Family::gett:
+      for (const auto& r : p.gett.rows) {
+        launches += 1 + (p.gett.pack_a ? 1 : 0) + (p.gett.pack_b ? 1 : 0);
+        if (r.a_alpha >= 0 || r.b_alpha >= 0) launches += 2;
+      }
+      break;
+    case Family::generic: launches += 1; break;
+  }
+  v.set("launches", Value::num(launches));
   Value leaves = Value::arr();
   for (const auto& L : p.leaves) {
     Value x = feinsum::transport::meta_to_json(L.meta);

@@ -119,6 +119,31 @@ class IRSearch {
     words_ = (static_cast<size_t>(n_) * n_ + 63) / 64;
   }
 
+  // adds a candidate automorphism after checking it on the adjacency lists
+  bool seed(const ColoredDigraph& g, const std::vector<int>& a) {
+    if (static_cast<int>(a.size()) != n_) return false;
+    std::vector<char> hit(static_cast<size_t>(n_), 0);
+    bool identity = true;
+    for (int v = 0; v < n_; ++v) {
+      const int w = a[v];
+      if (w < 0 || w >= n_ || hit[w] || g.colors[w] != g.colors[v]) return false;
+      hit[w] = 1;
+      identity = identity && w == v;
+    }
+    if (identity) return false;
+    std::size_t edges = 0;
+    for (int v = 0; v < n_; ++v) {
+      const std::uint8_t* row = &g.adj[static_cast<size_t>(a[v]) * n_];
+      for (int u : out_[v]) {
+        if (!row[a[u]]) return false;
+        ++edges;
+      }
+    }
+    (void)edges;  // a bijection mapping every edge onto an edge preserves the edge set
+    autos_.push_back(a);
+    return true;
+  }
+
   std::vector<int> run(const ColoredDigraph& g) {
     // initial partition by colour value, ascending
     std::vector<int> nodes(static_cast<size_t>(n_));
@@ -300,12 +325,15 @@ class IRSearch {
 
 }  // namespace
 
-Relabeling canonical_labeling(const ColoredDigraph& g) {
+Relabeling canonical_labeling(const ColoredDigraph& g) { return canonical_labeling(g, {}); }
+
+Relabeling canonical_labeling(const ColoredDigraph& g, const std::vector<std::vector<int>>& known_automorphisms) {
   if (g.n == 0) return Relabeling{{}};
   if (static_cast<int>(g.colors.size()) != g.n ||
       g.adj.size() != static_cast<size_t>(g.n) * static_cast<size_t>(g.n))
     throw error(errc::domain, "malformed colored digraph");
   IRSearch s(g);
+  for (const auto& a : known_automorphisms) s.seed(g, a);
   return Relabeling{s.run(g)};
 }
 

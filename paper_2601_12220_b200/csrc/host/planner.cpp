@@ -613,7 +613,17 @@ bool bind_gett(Plan& p, std::string* why) {
       *why = "batch index";
       return false;
     }
-  const std::string ni = c.i_out.back();
+  // ni: the kernel's inner N index (one 72-row TMA box per no value); the
+  // output's last index when its extent fits a box (coalesced C stores),
+  // else the next output index from the end that does
+  const auto lens0 = feinsum::index_lengths(c);
+  auto fits = [&](const std::string& x) { return lens0.at(x) >= 24 && lens0.at(x) <= 72; };
+  std::string ni = c.i_out.back();
+  for (auto it = c.i_out.rbegin(); it != c.i_out.rend(); ++it)
+    if (fits(*it)) {
+      ni = *it;
+      break;
+    }
   const int sb = s1.count(ni) ? 1 : 0, sa = 1 - sb;
   const feinsum::IndexList& la = c.i_in[sa];
   const feinsum::IndexList& lb = c.i_in[sb];
@@ -643,7 +653,7 @@ bool bind_gett(Plan& p, std::string* why) {
   for (const auto& x : lb)
     if (!K.count(x)) N.push_back(x);
   std::string mi = M[1], mo = M[0];  // later position = smaller stride in A
-  if (!a_ok && lens.at(mi) != 72 && lens.at(mo) == 72) std::swap(mi, mo);  // packed A: any order
+  if (!fits(mi) && fits(mo)) std::swap(mi, mo);  // TMA dims take any order
   const std::string no = N[0] == ni ? N[1] : N[0];
   GettBinding g;
   g.pack_a = !a_ok;
@@ -655,7 +665,7 @@ bool bind_gett(Plan& p, std::string* why) {
   g.ext_ka = lens.at(ka);
   g.ext_kb = lens.at(kb);
   if (!gett_supported(g.ext_mi, g.ext_ni, g.ext_ka, g.ext_kb)) {
-    *why = "extents outside the compiled 72x72 tile";
+    *why = "extents outside the kernel box (mi, ni in 24..72, even K extents)";
     return false;
   }
   auto stride_of = [&](const feinsum::IndexList& l, const std::vector<std::int64_t>& shape, const std::string& s) {
@@ -668,6 +678,10 @@ bool bind_gett(Plan& p, std::string* why) {
   const auto& shb = c.args[0][sb].shape;
   std::vector<std::int64_t> shc;
   for (const auto& s : c.i_out) shc.push_back(lens.at(s));
+  // TMA strides must be multiples of 16 bytes: an operand with an odd stride
+  // is repacked like a non-compliant one
+  if (!g.pack_a && (stride_of(la, sha, mo) % 2 || stride_of(la, sha, mi) % 2 || stride_of(la, sha, kb) % 2)) g.pack_a = true;
+  if (!g.pack_b && (stride_of(lb, shb, no) % 2 || stride_of(lb, shb, ni) % 2 || stride_of(lb, shb, ka) % 2)) g.pack_b = true;
   if (g.pack_a) {
     const std::int64_t src[4] = {stride_of(la, sha, mo), stride_of(la, sha, mi), stride_of(la, sha, kb),
                                  stride_of(la, sha, ka)};

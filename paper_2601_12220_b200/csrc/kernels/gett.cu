@@ -61,6 +61,7 @@ struct GettDev {
   const double* rowA;  // sum_k A[m, k] per (mo, mi) (affine operands only)
   const double* rowB;  // sum_k B[k, n] per (no, ni)
   std::int64_t ext_mi, ext_ni;
+  int vec_c;  // C rows allow 16-byte stores of (n, n+1) pairs
   double kdim;         // |K| = ext_ka * ext_kb
   int stages, group;  // group: side of the square raster block (tiles sharing A/B slices in L2)
 };
@@ -203,30 +204,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
     }
 
-    // epilogue: fragment (row qrow, cols 2*qk, 2*qk+1) of each 8x8 block
+    // epilogue: fragment (row qrow, cols 2*qk, 2*qk+1) of each 8x8 block;
+    // rows / columns beyond ext_mi / ext_ni (a box of 72 over a shorter
+    // extent, filled with zeros by TMA) are not stored
     const std::int64_t gmo = mo * MT + mo_l, gno = no * NT + wn;
     if (gmo >= p.ext_mo || gno >= p.ext_no) continue;
     double* cbase = p.C + gmo * p.c_mo + gno * p.c_no;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       const int m = m0 + i * 8 + qrow;
+      if (m >= p.ext_mi) continue;
       const double ra = (affine && bB != 0.0) ? p.rowA[gmo * p.ext_mi + m] : 0.0;
 #pragma unroll
       for (int j = 0; j < 9; ++j) {
         const int n = j * 8 + 2 * qk;
+        if (n >= p.ext_ni) continue;
+        const bool pair = n + 1 < p.ext_ni;
         double* dst = cbase + m * p.c_mi + n * p.c_ni;
         if (affine) {
           const double k = bA * bB * p.kdim;
           for (int v = 0; v < 2; ++v) {
-            const double rb = (bA != 0.0) ? p.rowB[gno * p.ext_ni + n + v] : 0.0;
+            const double rb = (bA != 0.0 && n + v < p.ext_ni) ? p.rowB[gno * p.ext_ni + n + v] : 0.0;
             acc[i][j][v] = fma(aA * aB, acc[i][j][v], fma(aA * bB, ra, fma(bA * aB, rb, k)));
           }
         }
-        if (p.c_ni == 1) {
+        if (p.vec_c && pair) {
           __stcs(reinterpret_cast<double2*>(dst), make_double2(acc[i][j][0], acc[i][j][1]));
         } else {
           dst[0] = acc[i][j][0];
-          dst[p.c_ni] = acc[i][j][1];
+          if (pair) dst[p.c_ni] = acc[i][j][1];
         }
       }
     }
@@ -280,8 +286,14 @@ bool make_map(CUtensorMap* map, const double* base, const std::uint64_t dims[4],
 
 }  // namespace
 
+// Extents up to one 72-row box per mo / no value (shorter ones are padded
+// with zeros by TMA and masked in the epilogue; K extents of any length, the
+// last k box likewise zero-padded). Even unit-stride extents keep every TMA
+// stride a multiple of 16 bytes; below a third of a box the generic kernel
+// is the better choice.
 bool gett_supported(std::int64_t ext_mi, std::int64_t ext_ni, std::int64_t ext_ka, std::int64_t ext_kb) {
-  return ext_mi == EXT && ext_ni == EXT && ext_ka % KA == 0 && ext_kb % KB == 0;
+  return ext_mi >= 24 && ext_mi <= EXT && ext_ni >= 24 && ext_ni <= EXT && ext_ka % 2 == 0 && ext_kb % 2 == 0 &&
+         ext_ka * ext_kb >= 64;
 }
 
 int launch_gett(const GettLaunch& L, void* stream) {
@@ -308,8 +320,10 @@ int launch_gett(const GettLaunch& L, void* stream) {
   d.no = (L.ext_no + NT - 1) / NT;
   d.ext_mo = L.ext_mo;
   d.ext_no = L.ext_no;
-  d.ka_steps = L.ext_ka / KA;
-  d.kb_steps = L.ext_kb / KB;
+  d.ka_steps = (L.ext_ka + KA - 1) / KA;
+  d.kb_steps = (L.ext_kb + KB - 1) / KB;
+  d.vec_c = L.c_ni == 1 && L.c_mi % 2 == 0 && L.c_mo % 2 == 0 && L.c_no % 2 == 0 &&
+            (reinterpret_cast<std::uintptr_t>(L.C) & 15) == 0;
   d.c_mo = L.c_mo;
   d.c_mi = L.c_mi;
   d.c_no = L.c_no;

@@ -447,3 +447,33 @@ def test_execute_host_pipelined(fe, torch_cuda, name):
         torch.cuda.synchronize()
         for g, w in zip(hout, want):
             assert torch.equal(g, w.cpu()), name
+
+
+@pytest.mark.parametrize("spec", [
+    # (A subscripts, B subscripts, extents a b c d e f, expect the DMMA kernel)
+    ("aebf", "dfce", (5, 40, 7, 50, 14, 18), True),   # short boxes, K tails (18 % 8, 14 % 4)
+    ("aebf", "fdec", (3, 72, 4, 33, 10, 22), True),   # repacked B, odd ni
+    ("eafd", "fbec", (30, 6, 5, 26, 8, 6), False),    # no M index fits a box: generic kernel
+    ("aebf", "dfce", (2, 90, 3, 60, 8, 8), False),    # b = 90 > 72 and a = 2: generic kernel
+])
+def test_gett_general_extents_exact(fe, torch_cuda, spec):
+    """GETT beyond extent 72: mi / ni boxes shorter than 72 (TMA zero fill,
+    masked epilogue), K extents that are not box multiples, repacked operands;
+    exact on dyadic data against fp64 torch.einsum. Shapes the kernel cannot
+    take (an M/N extent above 72 with no alternative) stay on the generic
+    kernel and are still correct."""
+    torch = torch_cuda
+    sa, sb, ext, dmma = spec
+    lens = dict(zip("abcdef", ext))
+    m = lambda n, s: {"name": n, "shape": [lens[x] for x in s], "dtype": "float64"}
+    e = {"i_out": list("abcd"), "i_in": [list(sa), list(sb)], "args": [[m("A", sa), m("B", sb)]]}
+    plan = fe.Plan(einsum=e)
+    A = torch.empty([lens[x] for x in sa], dtype=torch.float64, device="cuda")
+    B = torch.empty([lens[x] for x in sb], dtype=torch.float64, device="cuda")
+    fe.fill_dyadic(A, 5)
+    fe.fill_dyadic(B, 6)
+    (out,) = plan(A, B)
+    want = torch.einsum(f"{sa},{sb}->abcd", A, B)
+    torch.cuda.synchronize()
+    assert torch.equal(out, want), (spec, plan.info["transform"])
+    assert (plan.info["transform"] == "gett_dmma/v1") == dmma, plan.info

@@ -750,8 +750,8 @@ bool bind_tt(Plan& p, std::string* why) {
   t.NJ = static_cast<int>(lens.at(m->idx.at('j')));
   t.NK = static_cast<int>(lens.at(m->idx.at('k')));
   t.NL = static_cast<int>(lens.at(m->idx.at('l')));
-  if (!tt_supported(t.NI, t.NJ, t.NK, t.NL)) {
-    *why = "cores are not 64x64";
+  if (!tt_supported(t.NI, t.NJ, t.NK, t.NL, false) && !tt_supported(t.NI, t.NJ, t.NK, t.NL, true)) {
+    *why = "cores outside 8..64 (or an odd unit-stride extent)";
     return false;
   }
   const int n = p.skel.n();
@@ -782,6 +782,10 @@ bool bind_tt(Plan& p, std::string* why) {
     t.rows.push_back(r);
   }
   t.fp32 = storage == ST_F32;
+  if (!tt_supported(t.NI, t.NJ, t.NK, t.NL, t.fp32)) {
+    *why = "fp32 cores need a unit-stride extent divisible by 4";
+    return false;
+  }
   p.tt = std::move(t);
   return true;
 }

@@ -231,7 +231,7 @@ struct TTLaunch {
 };
 
 int launch_tt(const TTLaunch& p, void* stream);
-bool tt_supported(int NI, int NJ, int NK, int NL);
+bool tt_supported(int NI, int NJ, int NK, int NL, bool fp32);
 // fp32 on the tcgen05 tensor cores (3xTF32), tt_tc.cu
 int launch_tt_tc(const TTLaunch& p, void* stream);
 bool tt_tc_supported(const TTLaunch& p);

@@ -86,6 +86,7 @@ __device__ __forceinline__ int chunk_k0(int kp) { return (kp >> 2) * 16 + (kp & 
 
 struct TTDev {
   std::int64_t nb;
+  int NI, NJ, NK, NL;  // cores up to 64 x 64, zero-padded to the 64 x 64 tiles
   const void* G1;
   const void* G2;
   void* Y;
@@ -160,8 +161,9 @@ __global__ void __launch_bounds__(TTShape<T>::kThreadsT, 1)
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const int t = threadIdx.x + k * SH::kThreadsT;
-      v1[k] = static_cast<double>(__ldg(static_cast<const T*>(p.G1) + t));
-      v2[k] = static_cast<double>(__ldg(static_cast<const T*>(p.G2) + t));
+      const int r = t / R, c = t % R;
+      v1[k] = r < p.NI && c < p.NJ ? static_cast<double>(__ldg(static_cast<const T*>(p.G1) + r * p.NJ + c)) : 0.0;
+      v2[k] = r < p.NK && c < p.NL ? static_cast<double>(__ldg(static_cast<const T*>(p.G2) + r * p.NL + c)) : 0.0;
     }
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
@@ -250,16 +252,22 @@ __global__ void __launch_bounds__(TTShape<T>::kThreadsT, 1)
     const std::int64_t n = pr * kPair + smp;
     if (n < p.nb) {
       T* y = static_cast<T*>(p.Y) + n * p.y_sn;
+      const bool full = p.NI == R && p.NK == R;
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const int i = r2 + a * 8 + qr, k = c2 + b * 8 + 2 * qk;
-          if constexpr (sizeof(T) == 8) {
-            __stcs(reinterpret_cast<double2*>(y + i * R + k), make_double2(acc[a][b][0], acc[a][b][1]));
-          } else {
-            __stcs(reinterpret_cast<float2*>(y + i * R + k),
-                   make_float2(static_cast<float>(acc[a][b][0]), static_cast<float>(acc[a][b][1])));
+          if (full) {
+            if constexpr (sizeof(T) == 8) {
+              __stcs(reinterpret_cast<double2*>(y + i * R + k), make_double2(acc[a][b][0], acc[a][b][1]));
+            } else {
+              __stcs(reinterpret_cast<float2*>(y + i * R + k),
+                     make_float2(static_cast<float>(acc[a][b][0]), static_cast<float>(acc[a][b][1])));
+            }
+          } else if (i < p.NI) {  // padded core: rows / columns beyond the real extents are zeros
+            if (k < p.NK) y[i * p.NK + k] = static_cast<T>(acc[a][b][0]);
+            if (k + 1 < p.NK) y[i * p.NK + k + 1] = static_cast<T>(acc[a][b][1]);
           }
         }
     }
@@ -287,7 +295,7 @@ int launch_t(const TTLaunch& L, cudaStream_t stream) {
   if (!enc) return cudaErrorInvalidValue;
   CUtensorMap tm;
   // X viewed as (l, j, n): unit stride l, then j, then the sample stride
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(L.Nb)};
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(L.NL), static_cast<cuuint64_t>(L.NJ), static_cast<cuuint64_t>(L.Nb)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(L.x_sj * sizeof(T)), static_cast<cuuint64_t>(L.x_sn * sizeof(T))};
   cuuint32_t box[3] = {static_cast<cuuint32_t>(PT::P), static_cast<cuuint32_t>(R), 1};
   cuuint32_t es[3] = {1, 1, 1};
@@ -298,6 +306,10 @@ int launch_t(const TTLaunch& L, cudaStream_t stream) {
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   TTDev d{};
   d.nb = L.Nb;
+  d.NI = L.NI;
+  d.NJ = L.NJ;
+  d.NK = L.NK;
+  d.NL = L.NL;
   d.G1 = L.G1;
   d.G2 = L.G2;
   d.Y = L.Y;
@@ -316,10 +328,16 @@ int launch_t(const TTLaunch& L, cudaStream_t stream) {
 
 }  // namespace
 
-bool tt_supported(int NI, int NJ, int NK, int NL) { return NI == R && NJ == R && NK == R && NL == R; }
+// cores up to 64 x 64 (padded with zeros to the kernel's 64 x 64 tiles: the
+// X boxes by TMA out-of-bounds fill, G1/G2 when staged, Y masked); the
+// unit-stride extent NL must keep the TMA strides 16-byte multiples
+bool tt_supported(int NI, int NJ, int NK, int NL, bool fp32) {
+  return NI >= 8 && NI <= R && NJ >= 8 && NJ <= R && NK >= 8 && NK <= R && NL >= 8 && NL <= R &&
+         NL % (fp32 ? 4 : 2) == 0;
+}
 
 int launch_tt(const TTLaunch& L, void* stream) {
-  if (!tt_supported(L.NI, L.NJ, L.NK, L.NL) || L.Nb <= 0) return L.Nb == 0 ? cudaSuccess : cudaErrorInvalidValue;
+  if (!tt_supported(L.NI, L.NJ, L.NK, L.NL, L.fp32 != 0) || L.Nb <= 0) return L.Nb == 0 ? cudaSuccess : cudaErrorInvalidValue;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return L.fp32 ? launch_t<float>(L, s) : launch_t<double>(L, s);
 }

@@ -446,7 +446,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tc_encoder() {
 }  // namespace
 
 bool tt_tc_supported(const TTLaunch& L) {
-  return L.fp32 && tt_supported(L.NI, L.NJ, L.NK, L.NL) && L.x_sj == R && L.x_sn == R * R && L.y_sn == R * R &&
+  return L.fp32 && L.NI == R && L.NJ == R && L.NK == R && L.NL == R && L.x_sj == R && L.x_sn == R * R && L.y_sn == R * R &&
          (reinterpret_cast<std::uintptr_t>(L.X) & 15) == 0 && (reinterpret_cast<std::uintptr_t>(L.Y) & 15) == 0;
 }
 

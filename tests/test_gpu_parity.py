@@ -477,3 +477,33 @@ def test_gett_general_extents_exact(fe, torch_cuda, spec):
     torch.cuda.synchronize()
     assert torch.equal(out, want), (spec, plan.info["transform"])
     assert (plan.info["transform"] == "gett_dmma/v1") == dmma, plan.info
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 16, 16), (32, 48, 24, 40), (64, 40, 64, 56), (50, 8, 20, 12)])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_tensor_train_padded_cores(fe, torch_cuda, dims, dtype):
+    """TT cores smaller than 64 x 64 (and non-square) run the DMMA kernel on
+    zero-padded tiles; against an fp64 torch.einsum (fp32: the fp32 bar)."""
+    torch = torch_cuda
+    NI, NJ, NK, NL = dims
+    n = 37  # odd: a half-filled last pair
+    m = lambda name, s: {"name": name, "shape": list(s), "dtype": dtype}
+    e = {"i_out": ["n", "i", "k"], "i_in": [["i", "j"], ["k", "l"], ["n", "j", "l"]],
+         "args": [[m("G1", (NI, NJ)), m("G2", (NK, NL)), m("X", (n, NJ, NL))]]}
+    plan = fe.Plan(einsum=e)
+    assert plan.info["transform"] == "tt/v1", plan.info
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    G1 = torch.randn(NI, NJ, dtype=tdt, device="cuda")
+    G2 = torch.randn(NK, NL, dtype=tdt, device="cuda")
+    X = torch.randn(n, NJ, NL, dtype=tdt, device="cuda")
+    names = [mm["name"] for mm in plan.inputs]
+    ins = {"G1": G1, "G2": G2, "X": X}
+    (Y,) = plan(*[ins[k] for k in names])
+    want = torch.einsum("ij,kl,njl->nik", G1.double(), G2.double(), X.double())
+    err = ((Y.double() - want).abs() / want.abs().clamp(min=1.0)).max().item()
+    if dtype == "float64":
+        assert err <= FP64_TOL, err
+    else:
+        f32 = torch.einsum("ij,kl,njl->nik", G1, G2, X)
+        err_f32 = ((f32.double() - want).abs() / want.abs().clamp(min=1.0)).max().item()
+        assert err <= max(1e-5, 4 * err_f32), (err, err_f32)

@@ -1438,7 +1438,7 @@ std::string describe(const Plan& p) {
   int launches = p.chains.empty() ? 0 : 1;
   switch (p.family) {
     case Family::fem_grad: launches += 1; break;
-    case Family::hex: launches += 1; break;
+    case Family::hex: launches += (meta_int(p.meta, "v", 2) == 1 && p.hex.P == 5) ? 1 : 2; break;  // v2: + operator gather
     case Family::tt: launches += static_cast<int>(p.tt.rows.size()); break;
     case Family::gett:
       for (const auto& r : p.gett.rows) {

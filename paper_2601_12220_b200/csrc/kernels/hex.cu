@@ -293,16 +293,24 @@ __global__ void __launch_bounds__(kThreads, 2) hex_kernel(const __grid_constant_
 //   B  line (k,l) over j, two fields per thread:      F1[y] along j, q_x = G t_y,
 //                                                      B1[x]^T along a (G read once per two fields)
 //   C  plane i (b,c), one direction x per warp:       B2[x]^T along b, B3[x]^T along c
-//   S  row (i,m): y = sum_x partial_x, streamed to HBM
-// 3187 shared doubles per (element, field) against 12375 DFMA (v1: 5250 plus
-// operator loads). Work cubes (cube = field * 2 + element) sit 137 doubles
-// apart; with cube-fastest lanes in A and C and line-fastest lanes in B every
-// W access is conflict-free (two wavefronts per warp-wide 8-byte access);
-// only B's G reads keep a 2-way conflict where a half-warp spans both elements.
-__constant__ double c_hex_ops[6][ND][P2];
-// W cube stride: odd (plane accesses of cube-fastest lanes hit distinct banks)
-// and 9 mod 16 (consecutive lines of consecutive cubes continue the bank walk)
-constexpr int CS2 = 137;  // F1 F2 F3 B1 B2 B3, [d][o][i] as stored
+//   S  y = sum_x partial_x into a staging tile, one bulk store per field
+// At Q = 5: 3187 shared doubles per (element, field) against 12375 DFMA (v1:
+// 5250 plus operator loads). Work cubes (cube = field * NE + element) sit CS
+// doubles apart: odd, so the plane accesses of cube-fastest lanes in A and C
+// hit distinct banks, and (where Q^2 is odd) CS = Q^2 mod 16 so consecutive
+// line groups of B continue the bank walk. The kernel is templated on the
+// number of points per direction Q (3..6: P2..P5 hex elements).
+constexpr int kMaxQ = 6;
+// F1 F2 F3 B1 B2 B3 packed as stored: matrix k, direction d, entry (o, i) at
+// (k * ND + d) * Q^2 + o * Q + i (one copy per matrix per launch)
+__constant__ double c_hex_ops[6 * ND * kMaxQ * kMaxQ];
+
+template <int Q>
+struct Hx {
+  static constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
+  static constexpr int CS = Q == 3 ? 41 : Q == 4 ? 65 : Q == 5 ? 137 : 217;
+  static_assert(CS >= Q3 && CS % 2 == 1, "cube stride");
+};
 
 struct Hex2Dev {
   std::int64_t E;
@@ -313,129 +321,131 @@ struct Hex2Dev {
 };
 
 // forward operator entry M[o][i] = F[o][i]; backward M[o][i] = B[i][o]
-template <int K, int D, bool kBack>
+template <int Q, int K, int D, bool kBack>
 __device__ __forceinline__ double cop(int o, int i) {
-  return kBack ? c_hex_ops[K][D][i * P + o] : c_hex_ops[K][D][o * P + i];
+  constexpr int base = (K * ND + D) * Q * Q;
+  return kBack ? c_hex_ops[base + i * Q + o] : c_hex_ops[base + o * Q + i];
 }
 
-template <int K, int D, bool kBack>
-__device__ __forceinline__ void rows_c(double (&v)[P][P]) {
+template <int Q, int K, int D, bool kBack>
+__device__ __forceinline__ void rows_c(double (&v)[Q][Q]) {
 #pragma unroll
-  for (int r = 0; r < P; ++r) {
-    double o[P];
+  for (int r = 0; r < Q; ++r) {
+    double o[Q];
 #pragma unroll
-    for (int a = 0; a < P; ++a) {
-      double s = cop<K, D, kBack>(a, 0) * v[r][0];
+    for (int a = 0; a < Q; ++a) {
+      double s = cop<Q, K, D, kBack>(a, 0) * v[r][0];
 #pragma unroll
-      for (int b = 1; b < P; ++b) s = fma(cop<K, D, kBack>(a, b), v[r][b], s);
+      for (int b = 1; b < Q; ++b) s = fma(cop<Q, K, D, kBack>(a, b), v[r][b], s);
       o[a] = s;
     }
 #pragma unroll
-    for (int a = 0; a < P; ++a) v[r][a] = o[a];
+    for (int a = 0; a < Q; ++a) v[r][a] = o[a];
   }
 }
 
-template <int K, int D, bool kBack>
-__device__ __forceinline__ void cols_c(double (&v)[P][P]) {
+template <int Q, int K, int D, bool kBack>
+__device__ __forceinline__ void cols_c(double (&v)[Q][Q]) {
 #pragma unroll
-  for (int col = 0; col < P; ++col) {
-    double o[P];
+  for (int col = 0; col < Q; ++col) {
+    double o[Q];
 #pragma unroll
-    for (int a = 0; a < P; ++a) {
-      double s = cop<K, D, kBack>(a, 0) * v[0][col];
+    for (int a = 0; a < Q; ++a) {
+      double s = cop<Q, K, D, kBack>(a, 0) * v[0][col];
 #pragma unroll
-      for (int b = 1; b < P; ++b) s = fma(cop<K, D, kBack>(a, b), v[b][col], s);
+      for (int b = 1; b < Q; ++b) s = fma(cop<Q, K, D, kBack>(a, b), v[b][col], s);
       o[a] = s;
     }
 #pragma unroll
-    for (int a = 0; a < P; ++a) v[a][col] = o[a];
+    for (int a = 0; a < Q; ++a) v[a][col] = o[a];
   }
 }
 
 // pass A: u plane j -> t_y plane j (F3[y] along l, F2[y] along k)
-template <int Y>
+template <int Q, int Y>
 __device__ __forceinline__ void pass_a(const double* in, double* out) {
-  double v[P][P];
+  double v[Q][Q];
 #pragma unroll
-  for (int k = 0; k < P; ++k)
+  for (int k = 0; k < Q; ++k)
 #pragma unroll
-    for (int l = 0; l < P; ++l) v[k][l] = in[k * P + l];
-  rows_c<2, Y, false>(v);
-  cols_c<1, Y, false>(v);
+    for (int l = 0; l < Q; ++l) v[k][l] = in[k * Q + l];
+  rows_c<Q, 2, Y, false>(v);
+  cols_c<Q, 1, Y, false>(v);
 #pragma unroll
-  for (int b = 0; b < P; ++b)
+  for (int b = 0; b < Q; ++b)
 #pragma unroll
-    for (int c = 0; c < P; ++c) out[b * P + c] = v[b][c];
+    for (int c = 0; c < Q; ++c) out[b * Q + c] = v[b][c];
 }
 
 // pass C: q'_x plane i -> partial y_x plane i (B2[x]^T along b, B3[x]^T along c)
-template <int X>
+template <int Q, int X>
 __device__ __forceinline__ void pass_c(double* io) {
-  double v[P][P];
+  double v[Q][Q];
 #pragma unroll
-  for (int b = 0; b < P; ++b)
+  for (int b = 0; b < Q; ++b)
 #pragma unroll
-    for (int c = 0; c < P; ++c) v[b][c] = io[b * P + c];
-  cols_c<4, X, true>(v);
-  rows_c<5, X, true>(v);
+    for (int c = 0; c < Q; ++c) v[b][c] = io[b * Q + c];
+  cols_c<Q, 4, X, true>(v);
+  rows_c<Q, 5, X, true>(v);
 #pragma unroll
-  for (int m = 0; m < P; ++m)
+  for (int m = 0; m < Q; ++m)
 #pragma unroll
-    for (int n = 0; n < P; ++n) io[m * P + n] = v[m][n];
+    for (int n = 0; n < Q; ++n) io[m * Q + n] = v[m][n];
 }
 
 // F1[y] along j on one line (y compile-time)
-template <int Y>
-__device__ __forceinline__ void line_f1(double (&t)[P]) {
-  double o[P];
+template <int Q, int Y>
+__device__ __forceinline__ void line_f1(double (&t)[Q]) {
+  double o[Q];
 #pragma unroll
-  for (int a = 0; a < P; ++a) {
-    double s = cop<0, Y, false>(a, 0) * t[0];
+  for (int a = 0; a < Q; ++a) {
+    double s = cop<Q, 0, Y, false>(a, 0) * t[0];
 #pragma unroll
-    for (int j = 1; j < P; ++j) s = fma(cop<0, Y, false>(a, j), t[j], s);
+    for (int j = 1; j < Q; ++j) s = fma(cop<Q, 0, Y, false>(a, j), t[j], s);
     o[a] = s;
   }
 #pragma unroll
-  for (int a = 0; a < P; ++a) t[a] = o[a];
+  for (int a = 0; a < Q; ++a) t[a] = o[a];
 }
 
-// B1[x]^T along a on one line, stored with stride P2
-template <int X>
-__device__ __forceinline__ void line_b1(const double (&t)[P], double* out) {
+// B1[x]^T along a on one line, stored with stride Q^2
+template <int Q, int X>
+__device__ __forceinline__ void line_b1(const double (&t)[Q], double* out) {
 #pragma unroll
-  for (int i = 0; i < P; ++i) {
-    double s = cop<3, X, true>(i, 0) * t[0];
+  for (int i = 0; i < Q; ++i) {
+    double s = cop<Q, 3, X, true>(i, 0) * t[0];
 #pragma unroll
-    for (int a = 1; a < P; ++a) s = fma(cop<3, X, true>(i, a), t[a], s);
-    out[i * P2] = s;
+    for (int a = 1; a < Q; ++a) s = fma(cop<Q, 3, X, true>(i, a), t[a], s);
+    out[i * Hx<Q>::Q2] = s;
   }
 }
 
-// pass B on line (k,l) of NF fields: wl[f] = W + cube*P3 + kl (direction 0),
-// direction stride ds; g = Gs + el*P3 + kl with (x,y) block stride gs
-template <int NF>
+// pass B on line (k,l) of NF fields: wl[f] = W + cube*CS + kl (direction 0),
+// direction stride ds; g = Gs + el*Q3 + kl with (x,y) block stride gs
+template <int Q, int NF>
 __device__ __forceinline__ void pass_b(double* const (&wl)[NF], int ds, const double* g, int gs) {
-  double t[NF][ND][P];
+  constexpr int Q2 = Hx<Q>::Q2;
+  double t[NF][ND][Q];
 #pragma unroll
   for (int f = 0; f < NF; ++f)
 #pragma unroll
     for (int y = 0; y < ND; ++y)
 #pragma unroll
-      for (int j = 0; j < P; ++j) t[f][y][j] = wl[f][y * ds + j * P2];
+      for (int j = 0; j < Q; ++j) t[f][y][j] = wl[f][y * ds + j * Q2];
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
-    line_f1<0>(t[f][0]);
-    line_f1<1>(t[f][1]);
-    line_f1<2>(t[f][2]);
+    line_f1<Q, 0>(t[f][0]);
+    line_f1<Q, 1>(t[f][1]);
+    line_f1<Q, 2>(t[f][2]);
   }
   // q_x = sum_y G[x,y] t_y, pointwise; G read once for all NF fields
 #pragma unroll
-  for (int a = 0; a < P; ++a) {
+  for (int a = 0; a < Q; ++a) {
     double gv[ND][ND];
 #pragma unroll
     for (int x = 0; x < ND; ++x)
 #pragma unroll
-      for (int y = 0; y < ND; ++y) gv[x][y] = g[(x * ND + y) * gs + a * P2];
+      for (int y = 0; y < ND; ++y) gv[x][y] = g[(x * ND + y) * gs + a * Q2];
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       double q[ND];
@@ -451,29 +461,36 @@ __device__ __forceinline__ void pass_b(double* const (&wl)[NF], int ds, const do
   }
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
-    line_b1<0>(t[f][0], wl[f]);
-    line_b1<1>(t[f][1], wl[f] + ds);
-    line_b1<2>(t[f][2], wl[f] + 2 * ds);
+    line_b1<Q, 0>(t[f][0], wl[f]);
+    line_b1<Q, 1>(t[f][1], wl[f] + ds);
+    line_b1<Q, 2>(t[f][2], wl[f] + 2 * ds);
   }
 }
 
-// NE2 elements per stage, 128 NE2 threads: NE2 = 2 runs two CTAs per SM;
-// NE2 = 4 runs one CTA of 16 warps whose plane passes split into exactly five
-// direction-uniform warps per direction (no warp runs two code paths).
-template <int NE2>
-__global__ void __launch_bounds__(128 * NE2, NE2 == 2 ? 2 : 1) hex2_kernel(const __grid_constant__ Hex2Dev p) {
+// threads: the plane passes' 3 x NE x 8 x Q tasks (direction-major, so every
+// direction's tasks fill whole warps: at Q = 5, NE = 4 exactly five warps
+// each) plus one warp for the copy engine, idle in passes A and C
+template <int Q, int NE2>
+struct HexCfg {
+  static constexpr int kTasks = ND * NE2 * kMaxFields * Q;
+  static constexpr int kThreads = (kTasks + 31) / 32 * 32 + 32;
+};
+
+template <int Q, int NE2>
+__global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const __grid_constant__ Hex2Dev p) {
   constexpr int NE = NE2;
+  constexpr int Q2 = Hx<Q>::Q2, Q3 = Hx<Q>::Q3, CS = Hx<Q>::CS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);
   const int R = p.rows;
-  const int nblk = NE * R;   // cubes per pair, cube = field * NE + element
-  const int ds = nblk * CS2;  // direction stride in W
-  // layout (doubles): Gs[9][NE*P3] | Us[R][NE*P3] | W[ND][nblk][CS2] | Ys[R][NE*P3] | mbar {G, U}
+  const int nblk = NE * R;   // cubes per stage, cube = field * NE + element
+  const int ds = nblk * CS;  // direction stride in W
+  // layout (doubles): Gs[9][NE*Q3] | Us[R][NE*Q3] | W[ND][nblk][CS] | Ys[R][NE*Q3] | mbar {G, U}
   double* Gs = sm;
-  double* Us = Gs + ND * ND * NE * P3;
-  double* W = Us + R * NE * P3;
+  double* Us = Gs + ND * ND * NE * Q3;
+  double* W = Us + R * NE * Q3;
   double* Ys = W + ND * ds;  // output staging: one bulk store per field and stage
-  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(Ys + R * NE * P3);
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(Ys + R * NE * Q3);
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar[0], 1);
     ptx::mbar_init(&bar[1], 1);
@@ -481,93 +498,92 @@ __global__ void __launch_bounds__(128 * NE2, NE2 == 2 ? 2 : 1) hex2_kernel(const
   }
   __syncthreads();
 
-  const std::int64_t npairs = p.E / NE;
-  const std::uint32_t bytes = static_cast<std::uint32_t>(NE * P3 * 8);
-  auto issue_g = [&](std::int64_t pair) {
+  const std::int64_t nstages = p.E / NE;
+  const std::uint32_t bytes = static_cast<std::uint32_t>(NE * Q3 * 8);
+  auto issue_g = [&](std::int64_t st) {
     ptx::mbar_arrive_expect_tx(&bar[0], bytes * static_cast<std::uint32_t>(ND * ND));
-    const std::int64_t e0 = pair * NE;
+    const std::int64_t e0 = st * NE;
     for (int xy = 0; xy < ND * ND; ++xy)
-      ptx::bulk_g2s(Gs + xy * NE * P3, p.G + (xy * p.E + e0) * P3, bytes, &bar[0]);
+      ptx::bulk_g2s(Gs + xy * NE * Q3, p.G + (xy * p.E + e0) * Q3, bytes, &bar[0]);
   };
-  auto issue_u = [&](std::int64_t pair) {
+  auto issue_u = [&](std::int64_t st) {
     ptx::mbar_arrive_expect_tx(&bar[1], bytes * static_cast<std::uint32_t>(R));
-    const std::int64_t e0 = pair * NE;
-    for (int f = 0; f < R; ++f) ptx::bulk_g2s(Us + f * NE * P3, p.U[f] + e0 * P3, bytes, &bar[1]);
+    const std::int64_t e0 = st * NE;
+    for (int f = 0; f < R; ++f) ptx::bulk_g2s(Us + f * NE * Q3, p.U[f] + e0 * Q3, bytes, &bar[1]);
   };
-  // the copy engine is driven by lane 0 of the last warp, which has no pass-B
-  // work (and none in passes A/C at four elements per stage), so issuing the
-  // next stage's copies never delays a computing warp
+  // the copy engine is driven by lane 0 of the last warp, which has no work in
+  // passes A / C and none in B at the pinned config, so issuing the next
+  // stage's copies never delays a computing warp
   const bool producer = threadIdx.x == blockDim.x - 32;
-  if (producer && blockIdx.x < npairs) {
+  if (producer && blockIdx.x < nstages) {
     issue_u(blockIdx.x);
     issue_g(blockIdx.x);
   }
 
-  // passes A and C: thread -> (direction, cube, plane), direction slowest, so
-  // only the warps straddling a direction boundary run two code paths
-  const int dir = threadIdx.x / (nblk * P);
-  const int ptask = threadIdx.x - dir * nblk * P;
-  const bool pactive = dir < ND;
+  // passes A and C: thread -> (direction, cube, plane), direction slowest
+  const int dir = threadIdx.x / (nblk * Q);
+  const int ptask = threadIdx.x - dir * nblk * Q;
+  const bool pactive = dir < ND && threadIdx.x < blockDim.x - 32;
   const int pplane = ptask / nblk, pcube = ptask - pplane * nblk;  // cube fastest
-  const double* a_in = Us + pcube * P3 + pplane * P2;
-  double* a_out = W + dir * ds + pcube * CS2 + pplane * P2;
+  const double* a_in = Us + pcube * Q3 + pplane * Q2;
+  double* a_out = W + dir * ds + pcube * CS + pplane * Q2;
   // pass B: thread -> (line, element, field pair (f, f + H)), line fastest
   const int H = (R + 1) / 2;
-  const int nbt = H * NE * P2;
+  const int nbt = H * NE * Q2;
 
   int it = 0;
-  for (std::int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x, ++it) {
+  for (std::int64_t st = blockIdx.x; st < nstages; st += gridDim.x, ++it) {
     const std::uint32_t phase = static_cast<std::uint32_t>(it & 1);
-    const bool more = pair + gridDim.x < npairs;
+    const bool more = st + gridDim.x < nstages;
 
     ptx::mbar_wait(&bar[1], phase);
     if (pactive) {
-      if (dir == 0) pass_a<0>(a_in, a_out);
-      else if (dir == 1) pass_a<1>(a_in, a_out);
-      else pass_a<2>(a_in, a_out);
+      if (dir == 0) pass_a<Q, 0>(a_in, a_out);
+      else if (dir == 1) pass_a<Q, 1>(a_in, a_out);
+      else pass_a<Q, 2>(a_in, a_out);
     }
     __syncthreads();
-    if (producer && more) issue_u(pair + gridDim.x);
+    if (producer && more) issue_u(st + gridDim.x);
 
     ptx::mbar_wait(&bar[0], phase);
     for (int t = threadIdx.x; t < nbt; t += blockDim.x) {
-      const int kl = t % P2;
-      const int r = t / P2;
+      const int kl = t % Q2;
+      const int r = t / Q2;
       const int el = r % NE, f0 = r / NE, f1 = f0 + H;
-      const double* g = Gs + el * P3 + kl;
+      const double* g = Gs + el * Q3 + kl;
       // odd R: the last thread pairs its field with itself (same values
       // written twice by the same thread) — one code path, smaller kernel
-      double* const w0 = W + (f0 * NE + el) * CS2 + kl;
-      double* const wl[2] = {w0, f1 < R ? W + (f1 * NE + el) * CS2 + kl : w0};
-      pass_b<2>(wl, ds, g, NE * P3);
+      double* const w0 = W + (f0 * NE + el) * CS + kl;
+      double* const wl[2] = {w0, f1 < R ? W + (f1 * NE + el) * CS + kl : w0};
+      pass_b<Q, 2>(wl, ds, g, NE * Q3);
     }
     __syncthreads();
-    if (producer && more) issue_g(pair + gridDim.x);
+    if (producer && more) issue_g(st + gridDim.x);
 
     if (pactive) {
-      if (dir == 0) pass_c<0>(a_out);
-      else if (dir == 1) pass_c<1>(a_out);
-      else pass_c<2>(a_out);
+      if (dir == 0) pass_c<Q, 0>(a_out);
+      else if (dir == 1) pass_c<Q, 1>(a_out);
+      else pass_c<Q, 2>(a_out);
     }
     if (producer) ptx::bulk_wait_read<0>();  // the previous stage's stores have read Ys
     __syncthreads();
 
-    const std::int64_t e0 = pair * NE;
+    const std::int64_t e0 = st * NE;
     // sum the three direction partials into the staging tile (a field's
-    // stage output is one contiguous run of NE * P3 doubles), then one bulk
+    // stage output is one contiguous run of NE * Q3 doubles), then one bulk
     // copy per field streams it to HBM while the next stage computes —
     // instead of a burst of global stores at the end of every stage
-    for (int off = threadIdx.x; off < NE * P3; off += blockDim.x) {
-      const int el = off / P3;
-      const double* w = W + el * CS2 + (off - el * P3);
+    for (int off = threadIdx.x; off < NE * Q3; off += blockDim.x) {
+      const int el = off / Q3;
+      const double* w = W + el * CS + (off - el * Q3);
 #pragma unroll
       for (int f = 0; f < kMaxFields; ++f)
-        if (f < R) Ys[f * NE * P3 + off] = (w[f * NE * CS2] + w[ds + f * NE * CS2]) + w[2 * ds + f * NE * CS2];
+        if (f < R) Ys[f * NE * Q3 + off] = (w[f * NE * CS] + w[ds + f * NE * CS]) + w[2 * ds + f * NE * CS];
     }
     ptx::fence_proxy_async();
-    __syncthreads();  // W is rewritten by the next pair's pass A; Ys complete
+    __syncthreads();  // W is rewritten by the next stage's pass A; Ys complete
     if (producer) {
-      for (int f = 0; f < R; ++f) ptx::bulk_s2g(p.Y[f] + e0 * P3, Ys + f * NE * P3, bytes);
+      for (int f = 0; f < R; ++f) ptx::bulk_s2g(p.Y[f] + e0 * Q3, Ys + f * NE * Q3, bytes);
       ptx::bulk_commit();
     }
   }
@@ -578,16 +594,25 @@ __global__ void __launch_bounds__(128 * NE2, NE2 == 2 ? 2 : 1) hex2_kernel(const
 // waits for the previous one (any stream) before restaging them.
 struct HexConstSlot {
   cudaEvent_t last = nullptr;
+  double* stage = nullptr;  // device staging of the six operators (one constant copy per launch)
 };
+
+struct Mats6 {
+  const double* m[6];
+};
+__global__ void gather_ops(const __grid_constant__ Mats6 src, int n, double* dst) {
+  for (int t = threadIdx.x; t < 6 * n; t += blockDim.x) dst[t] = src.m[t / n][t % n];
+}
 std::mutex g_hex_mu;
 HexConstSlot g_hex_slot[64];
 
-template <int NE2>
+template <int Q, int NE2>
 int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
+  constexpr int Q2 = Hx<Q>::Q2, Q3 = Hx<Q>::Q3, CS = Hx<Q>::CS;
   const int R = L.rows;
   const int nblk = NE2 * R;
-  const int threads = 128 * NE2;  // >= ND * nblk * P plane tasks for R <= 8
-  auto kern = hex2_kernel<NE2>;
+  constexpr int threads = HexCfg<Q, NE2>::kThreads;
+  auto kern = hex2_kernel<Q, NE2>;
   Hex2Dev d{};
   d.E = L.E;
   d.rows = R;
@@ -596,7 +621,7 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
     d.U[f] = L.U[f];
     d.Y[f] = L.Y[f];
   }
-  const size_t doubles = ND * ND * NE2 * P3 + 2 * R * NE2 * P3 + ND * nblk * CS2;
+  const size_t doubles = ND * ND * NE2 * Q3 + 2 * R * NE2 * Q3 + ND * nblk * CS;
   const size_t smem = doubles * 8 + 16;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -614,33 +639,51 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
   HexConstSlot& slot = g_hex_slot[dev & 63];
   if (slot.last) cudaStreamWaitEvent(st, slot.last, 0);
   else if ((e = cudaEventCreateWithFlags(&slot.last, cudaEventDisableTiming)) != cudaSuccess) return e;
-  for (int k = 0; k < 6; ++k) {
-    e = cudaMemcpyToSymbolAsync(c_hex_ops, L.mats[k], ND * P2 * sizeof(double), k * ND * P2 * sizeof(double),
-                                cudaMemcpyDeviceToDevice, st);
-    if (e != cudaSuccess) return e;
-  }
+  // gather the six operators into one run, then one copy into the constant
+  // bank (each copy costs tens of microseconds of stream time)
+  if (!slot.stage && (e = cudaMalloc(&slot.stage, 6 * ND * kMaxQ * kMaxQ * sizeof(double))) != cudaSuccess) return e;
+  Mats6 m6{};
+  for (int k = 0; k < 6; ++k) m6.m[k] = L.mats[k];
+  gather_ops<<<1, 256, 0, st>>>(m6, ND * Q2, slot.stage);
+  e = cudaMemcpyToSymbolAsync(c_hex_ops, slot.stage, 6 * ND * Q2 * sizeof(double), 0, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
   kern<<<static_cast<int>(grid), threads, smem, st>>>(d);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return cudaEventRecord(slot.last, st);
 }
 
-// elements per stage: 4 when E allows (fact meta ne=2 forces the two-CTA form)
+// elements per stage: 4 when E allows (fact meta ne=2 forces two), 2 at Q = 6
+// (shared memory)
+template <int Q>
+int launch_hex2_q(const HexLaunch& L, cudaStream_t st) {
+  if constexpr (Q < 6) {
+    if (L.ne != 2 && L.E % 4 == 0) return launch_hex2_t<Q, 4>(L, st);
+  }
+  return launch_hex2_t<Q, 2>(L, st);
+}
+
 int launch_hex2(const HexLaunch& L, cudaStream_t st) {
-  if (L.ne != 2 && L.E % 4 == 0) return launch_hex2_t<4>(L, st);
-  return launch_hex2_t<2>(L, st);
+  switch (L.P) {
+    case 3: return launch_hex2_q<3>(L, st);
+    case 4: return launch_hex2_q<4>(L, st);
+    case 5: return launch_hex2_q<5>(L, st);
+    case 6: return launch_hex2_q<6>(L, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
+// v2 takes 3..6 points per direction (P2..P5 hexes), v1 only 5
 bool hex_supported(int nd, int p, std::int64_t E, int rows) {
-  return nd == ND && p == P && E % NE == 0 && rows >= 1 && rows <= kMaxFields;
+  return nd == ND && p >= 3 && p <= kMaxQ && E % NE == 0 && rows >= 1 && rows <= kMaxFields;
 }
 
 int launch_hex(const HexLaunch& L, void* stream) {
   if (!hex_supported(L.ND, L.P, L.E, L.rows)) return cudaErrorInvalidValue;
   if (L.E == 0) return cudaSuccess;
-  if (L.variant != 1) return launch_hex2(L, static_cast<cudaStream_t>(stream));
+  if (L.variant != 1 || L.P != P) return launch_hex2(L, static_cast<cudaStream_t>(stream));
   HexDev d{};
   d.E = L.E;
   d.rows = L.rows;

@@ -507,3 +507,29 @@ def test_tensor_train_padded_cores(fe, torch_cuda, dims, dtype):
         f32 = torch.einsum("ij,kl,njl->nik", G1, G2, X)
         err_f32 = ((f32.double() - want).abs() / want.abs().clamp(min=1.0)).max().item()
         assert err <= max(1e-5, 4 * err_f32), (err, err_f32)
+
+
+@pytest.mark.parametrize("Q", [3, 4, 6])
+def test_hex_other_orders(fe, torch_cuda, Q):
+    """The v2 hex kernel templated on the points per direction (P2, P3, P5
+    hexes besides C2's P4), shared and distinct operators, ragged element
+    counts (the two-element stage), against an fp64 torch.einsum."""
+    from paper_2601_12220_b200 import configs as C
+    torch = torch_cuda
+    for E, b, distinct in [(8, 3, True), (6, 8, False), (40, 5, True)]:
+        e = C.hex_poisson(E=E, b=b, P=Q, distinct=distinct)
+        plan = fe.Plan(einsum=e)
+        assert plan.info["transform"] == "hex_sumfact/v1", plan.info
+        ins = {}
+        for k, m in enumerate(plan.inputs):
+            t = torch.empty(m["shape"], dtype=torch.float64, device="cuda")
+            fe.fill_dyadic(t, 90 + k + Q)
+            ins[m["name"]] = t
+        outs = plan(*[ins[m["name"]] for m in plan.inputs])
+        A = [ins[f"A{d}"] for d in (1, 2, 3)]
+        F = [ins[f"F{d}"] for d in (1, 2, 3)] if distinct else A
+        for q in range(b):
+            want = torch.einsum("xai,xbm,xcn,xyeabc,yaj,ybk,ycl,ejkl->eimn", A[0], A[1], A[2], ins["G"], F[0], F[1], F[2],
+                                ins[f"u{q + 1}"])
+            err = ((outs[q] - want).abs() / want.abs().clamp(min=1.0)).max().item()
+            assert err <= FP64_TOL, (Q, E, b, q, err)

@@ -248,10 +248,16 @@ __global__ void rowsum_kernel(const double* __restrict__ X, double* __restrict__
   if (warp >= n0 * n1) return;
   const std::int64_t r0 = warp / n1, r1 = warp % n1;
   const double* base = X + r0 * s_r0 + r1 * s_r1;
-  double s = 0.0;
-  for (std::int64_t t = lane; t < m0 * m1; t += 32) s += __ldg(base + (t / m1) * s_c0 + (t % m1) * s_c1);
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) rows[warp] = s;
+  // nested loops (no division per element), four independent partial sums
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  int k = 0;
+  for (std::int64_t c0 = 0; c0 < m0; ++c0) {
+    const double* row = base + c0 * s_c0;
+    for (std::int64_t c1 = lane; c1 < m1; c1 += 32, k = (k + 1) & 3) s[k] += __ldg(row + c1 * s_c1);
+  }
+  double t = (s[0] + s[1]) + (s[2] + s[3]);
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) rows[warp] = t;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

@@ -966,9 +966,38 @@ void upload_tables(Plan& p, GenericLaunch& g, const BatchedEinsum& e, bool dry_r
   cuda_check(device_sm_count(&p.sm_count), "device attributes");
   cuda_check(cudaMalloc(&p.d_blob, total), "cudaMalloc(plan tables)");
   cuda_check(cudaMemcpy(p.d_blob, blob.data(), total, cudaMemcpyHostToDevice), "upload plan tables");
-  if (!p.chains.empty())
+  if (!p.chains.empty()) {
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_coef), sizeof(double) * 2 * p.chains.size()),
                "cudaMalloc(coefficients)");
+    // literal-only chains (e.g. C5's 0.5) are folded here with the coefficient
+    // kernel's arithmetic (complex left fold, IEEE products, no contraction)
+    // and uploaded once, which saves a launch per execute
+    bool literal = true;
+    for (const auto& ch : p.chains)
+      for (int f = 0; f < ch.n; ++f) literal = literal && ch.f[f].leaf < 0;
+    if (literal) {
+      std::vector<double> host(2 * p.chains.size());
+      for (size_t c = 0; c < p.chains.size(); ++c) {
+        double re = 0.0, im = 0.0;
+        for (int f = 0; f < p.chains[c].n; ++f) {
+          const double vr = p.chains[c].f[f].lit, vi = 0.0;
+          if (f == 0) {
+            re = vr;
+            im = vi;
+          } else {
+            const double nr = re * vr - im * vi, ni = re * vi + im * vr;
+            re = nr;
+            im = ni;
+          }
+        }
+        host[2 * c] = re;
+        host[2 * c + 1] = im;
+      }
+      cuda_check(cudaMemcpy(p.d_coef, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice),
+                 "upload coefficients");
+      p.coef_static = true;
+    }
+  }
   auto* base = static_cast<unsigned char*>(p.d_blob);
   g.ops = reinterpret_cast<const OperandStatic*>(base + o_ops);
   g.slot_pos = reinterpret_cast<const int*>(base + o_pos);
@@ -1212,7 +1241,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
     g.leaves.storage[i] = plan.leaves[i].storage;
   }
   for (int r = 0; r < plan.skel.b(); ++r) g.out[r] = d_out[r];
-  if (!plan.chains.empty())
+  if (!plan.chains.empty() && !plan.coef_static)
     cuda_check(launch_coef(g.chains, g.n_chains, g.leaves, plan.d_coef, stream), "coefficient kernel");
 
   if (plan.family == Family::fem_grad) {
@@ -1408,7 +1437,7 @@ void tabulate(const Plan& plan, const std::string& name, const void* const* d_in
     t.leaves.storage[i] = plan.leaves[i].storage;
   }
   t.out = d_out;
-  if (!plan.chains.empty())
+  if (!plan.chains.empty() && !plan.coef_static)
     cuda_check(launch_coef(t.chains, t.n_chains, t.leaves, plan.d_coef, stream), "coefficient kernel");
   cuda_check(launch_tabulate(t, stream), "tabulate kernel");
 }
@@ -1435,7 +1464,7 @@ std::string describe(const Plan& p) {
   // kernels one execute launches (tuned path, aligned buffers): the family's
   // kernel per row where it loops over rows, plus the coefficient kernel and
   // GETT's operand passes (row sums for alpha*X+beta, repacks)
-  int launches = p.chains.empty() ? 0 : 1;
+  int launches = p.chains.empty() || p.coef_static ? 0 : 1;
   switch (p.family) {
     case Family::fem_grad: launches += 1; break;
     case Family::hex: launches += (meta_int(p.meta, "v", 2) == 1 && p.hex.P == 5) ? 1 : 2; break;  // v2: + operator gather

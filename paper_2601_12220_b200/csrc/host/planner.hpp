@@ -144,6 +144,7 @@ struct Plan {
   int device = 0;
   void* d_blob = nullptr;
   double* d_coef = nullptr;
+  bool coef_static = false;     // every chain is literal: coefficients uploaded once, no per-execute kernel
   double* d_scratch = nullptr;  // family workspace (GETT affine K-sums)
   double* d_pack_a = nullptr;   // GETT repacked operands (see GettBinding)
   double* d_pack_b = nullptr;

@@ -125,26 +125,30 @@ __global__ void __launch_bounds__(TTShape<T>::kThreadsT, 1)
   const int grp = warp / kConsumerWarps, wl = warp % kConsumerWarps;
   unsigned char* xs0 = g2 + PD::kBytes + grp * SH::kGroupBytes;  // this group's X pair
   if (threadIdx.x == 0) {
-    for (int g = 0; g < SH::kGroups; ++g) ptx::mbar_init(&full[g], 1);
+    for (int g = 0; g < SH::kGroups * kPair; ++g) ptx::mbar_init(&full[g], 1);
     ptx::fence_barrier_init();
   }
   __syncthreads();
 
   const std::int64_t npairs = (p.nb + kPair - 1) / kPair;
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * SH::kGroups;
-  const bool leader = wl == 0 && lane == 0;
+  // the two samples of a pair are independent (each sample's four warps own
+  // its GEMMs and its half of the stage): one mbarrier, one TMA issue and one
+  // named barrier per sample, so the samples drift apart and cover each
+  // other's barrier / store phases on the tensor pipe
+  const int smp = wl >> 2;
+  const bool leader = (wl & 3) == 0 && lane == 0;
+  std::uint64_t* fb = &full[grp * kPair + smp];
   auto issue = [&](std::int64_t pr) {
-    ptx::mbar_arrive_expect_tx(&full[grp], SH::kStageBytes);
-    for (int smp = 0; smp < kPair; ++smp)
-      for (int panel = 0; panel < R / PT::P; ++panel) {
-        unsigned char* dst = xs0 + smp * PT::kBytes + panel * PT::kPanelBytes;
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
-                ptx::smem_addr(dst)),
-            "l"(&tmX), "r"(ptx::smem_addr(&full[grp])), "r"(panel * PT::P), "r"(0),
-            "r"(static_cast<int>(pr * kPair + smp))
-            : "memory");
-      }
+    ptx::mbar_arrive_expect_tx(fb, PT::kBytes);
+    for (int panel = 0; panel < R / PT::P; ++panel) {
+      unsigned char* dst = xs0 + smp * PT::kBytes + panel * PT::kPanelBytes;
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+              ptx::smem_addr(dst)),
+          "l"(&tmX), "r"(ptx::smem_addr(fb)), "r"(panel * PT::P), "r"(0), "r"(static_cast<int>(pr * kPair + smp))
+          : "memory");
+    }
   };
   const std::int64_t first = static_cast<std::int64_t>(blockIdx.x) * SH::kGroups + grp;
   if (leader && first < npairs) {
@@ -173,11 +177,12 @@ __global__ void __launch_bounds__(TTShape<T>::kThreadsT, 1)
     }
   }
   __syncthreads();
-  auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kConsumerWarps * 32) : "memory"); };
+  auto group_sync = [&]() {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp * kPair + smp), "n"(kConsumerWarps / kPair * 32) : "memory");
+  };
 
   const int qr = lane >> 2, qk = lane & 3;
   // GEMM 1 tile: stacked rows [32*(w/2), +32) (sample (w/2)/2), cols [32*(w%2), +32)
-  const int smp = wl >> 2;
   const int r1 = (wl >> 1) * 32 - smp * R, c1 = (wl & 1) * 32;
   // GEMM 2 tile (same sample): rows i [32*(w%2), +32), cols k [32*((w>>1)&1), +32)
   const int r2 = (wl & 1) * 32, c2 = ((wl >> 1) & 1) * 32;
@@ -187,7 +192,7 @@ __global__ void __launch_bounds__(TTShape<T>::kThreadsT, 1)
   unsigned char* ts = SH::kInPlaceT ? xs : xs0 + SH::kStageBytes + smp * PD::kBytes;
   int it = 0;
   for (std::int64_t pr = first; pr < npairs; pr += stride, ++it) {
-    ptx::mbar_wait(&full[grp], it & 1u);
+    ptx::mbar_wait(fb, it & 1u);
 
     double acc[4][4][2];
 #pragma unroll

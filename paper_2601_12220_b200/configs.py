@@ -120,4 +120,19 @@ def wave_kernel(E=2_000_000, b=3, NX=3, NI=10, renamed=False):
     return "\n".join(lines) + "\n"
 
 
+def wave_kernel_nonlinear(E=2_000_000, b=3, NX=3, NI=10):
+    """The C5 skeleton with a non-affine stage operand
+    s_q = u_q^2 - sin(k_q) / (2 + exp(u_q)): evaluated by the device VM into a
+    table at the start of the execute, then read by the fem_grad kernel."""
+    lines = [f"domain: x<{NX} r<{NX} e<{E} i<{NI} j<{NI}"]
+    for q in range(1, b + 1):
+        lines.append(f"def s{q}(p,t) := u{q}[p,t]*u{q}[p,t] - sin(k{q}[p,t]) / (2 + exp(u{q}[p,t]))")
+    lines += [f"array: J float64 {NX}x{NX}x{E}", f"array: D float64 {NX}x{NI}x{NI}"]
+    for q in range(1, b + 1):
+        lines += [f"array: u{q} float64 {E}x{NI}", f"array: k{q} float64 {E}x{NI}"]
+    for q in range(1, b + 1):
+        lines.append(f"stmt y{q}[r,e,i] = sum([x,j], J[x,r,e]*D[x,i,j]*s{q}(e,j))")
+    return "\n".join(lines) + "\n"
+
+
 SUITE = ["C1", "C2", "C3", "C4-f64", "C4-f32", "C5"]

@@ -41,6 +41,11 @@ void cuda_check(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e
 
 }  // namespace
 
+const LeafInfo& leaf_info(const Plan& p, int i) {
+  const size_t n = p.leaves.size();
+  return static_cast<size_t>(i) < n ? p.leaves[static_cast<size_t>(i)] : p.tab_leaves.at(static_cast<size_t>(i) - n);
+}
+
 const char* family_transform(Family f) {
   switch (f) {
     case Family::generic: return "generic/v1";
@@ -112,6 +117,7 @@ PlanOptions parse_options(const std::string& json) {
   if (auto* x = v.find("canonicalize")) o.canonicalize = x->b;
   if (auto* x = v.find("dry_run")) o.dry_run = x->b;
   if (auto* x = v.find("meta")) o.meta_override = x->as_str();
+  if (auto* x = v.find("codegen")) o.codegen = x->b;
   return o;
 }
 
@@ -517,7 +523,7 @@ bool bind_fem(Plan& p, std::string* why) {
       *why = "functional J or D operand";
       return false;
     }
-    if (p.leaves[J.leaf].storage != ST_F64 || p.leaves[D.leaf].storage != ST_F64) {
+    if (leaf_info(p, J.leaf).storage != ST_F64 || leaf_info(p, D.leaf).storage != ST_F64) {
       *why = "non-f64 storage";
       return false;
     }
@@ -537,7 +543,7 @@ bool bind_fem(Plan& p, std::string* why) {
       return false;
     }
     for (const auto& t : terms)
-      if (p.leaves[t.leaf].storage != ST_F64) {
+      if (leaf_info(p, t.leaf).storage != ST_F64) {
         *why = "non-f64 storage";
         return false;
       }
@@ -584,7 +590,7 @@ bool gett_operand(const Plan& p, const OperandStatic& op, int* leaf, int* alpha,
   } else {
     return false;
   }
-  return p.leaves[*leaf].storage == ST_F64;
+  return leaf_info(p, *leaf).storage == ST_F64;
 }
 
 // GETT family: 2 slots, pure contraction (every index in exactly two of A, B,
@@ -766,7 +772,7 @@ bool bind_tt(Plan& p, std::string* why) {
         *why = "functional operand";
         return false;
       }
-      const int st = p.leaves[op.leaf].storage;
+      const int st = leaf_info(p, op.leaf).storage;
       if ((st != ST_F64 && st != ST_F32) || (storage >= 0 && st != storage)) {
         *why = "storage must be uniformly f64 or f32";
         return false;
@@ -825,7 +831,7 @@ bool bind_hex(Plan& p, std::string* why) {
     const int ur = p.canon.sigma_row[q];
     auto leaf_at = [&](int role) -> int {
       const OperandStatic& op = p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[m->slot[role]]];
-      if (op.kind != OPK_PLAIN || p.leaves[op.leaf].storage != ST_F64) return -1;
+      if (op.kind != OPK_PLAIN || leaf_info(p, op.leaf).storage != ST_F64) return -1;
       return op.leaf;
     };
     for (int role = 0; role < 8; ++role) {
@@ -1126,6 +1132,16 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
   }
   p.transform = family_transform(p.family);
   if (!opt.meta_override.empty()) p.meta = opt.meta_override;
+  if (p.family == Family::generic && !p.tabs.empty()) {
+    // the generic kernel evaluates the programs in place: no tables
+    const size_t bn = static_cast<size_t>(e.b()) * e.n(), nl = p.leaves.size();
+    for (size_t i = 0; i < bn; ++i)
+      if (p.ops[i].kind == OPK_PLAIN && static_cast<size_t>(p.ops[i].leaf) >= nl)
+        p.ops[i] = p.ops[static_cast<size_t>(p.tabs[static_cast<size_t>(p.ops[i].leaf) - nl].op)];
+    p.ops.resize(bn);
+    p.tabs.clear();
+    p.tab_leaves.clear();
+  }
 
   // generic launch (always prepared: it is also the runtime fallback)
   std::vector<std::string> syms = e.i_out;
@@ -1147,6 +1163,24 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
   for (int r = 0; r < e.b(); ++r) g.out_storage[r] = p.outputs[r].storage;
 
   upload_tables(p, g, e, opt.dry_run);
+  for (size_t k = 0; k < p.tabs.size(); ++k) {
+    Plan::TabOperand& t = p.tabs[k];
+    const std::string src = tab_kernel_source(p, p.ops[static_cast<size_t>(t.op)], p.tab_leaves[k].meta, &t.leaf_slots);
+    std::string log;
+    if (!opt.codegen)
+      t.codegen = "vm: codegen disabled";
+    else if (src.empty())
+      t.codegen = "vm: program not expressible (f16 leaf or > 16 leaves)";
+    else if (opt.dry_run)
+      t.codegen = nvrtc_compiles(src, &log) ? "nvrtc" : "vm: " + log.substr(0, 200);
+    else
+      t.codegen = (t.kernel = compile_tab_kernel(src, &log)) != nullptr ? "nvrtc" : "vm: " + log.substr(0, 200);
+  }
+  if (!opt.dry_run && !p.tabs.empty()) {
+    const Plan::TabOperand& last = p.tabs.back();
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_tab), sizeof(double) * static_cast<size_t>(last.offset + last.count)),
+               "cudaMalloc(tabulated operands)");
+  }
   if (!opt.dry_run && p.family == Family::gett) {
     bool affine = false;
     for (const auto& r : p.gett.rows) affine = affine || r.a_alpha >= 0 || r.b_alpha >= 0;
@@ -1181,6 +1215,7 @@ Plan::~Plan() {
   if (d_scratch) cudaFree(d_scratch);
   if (d_pack_a) cudaFree(d_pack_a);
   if (d_pack_b) cudaFree(d_pack_b);
+  if (d_tab) cudaFree(d_tab);
 }
 
 std::unique_ptr<Plan> make_plan(const BatchedEinsum& e, const PlanOptions& opt) {
@@ -1230,19 +1265,85 @@ std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,
   }
   for (int r = 0; r < skeleton.b(); ++r)
     for (int k = 0; k < skeleton.n(); ++k) p->ops.push_back(compiled.at(skeleton.args[r][k].name));
+  // real-valued VM operands become tabulated leaves (Plan::tabs); finish_plan
+  // drops them again if no tuned family binds
+  constexpr std::int64_t kTabBudget = std::int64_t{1} << 30;  // doubles (8 GiB)
+  if (!p->complex_mode && !opt.force_vm) {
+    std::int64_t off = 0;
+    for (const auto& m : feinsum::universe(skeleton)) {
+      const OperandStatic c = compiled.at(m.name);
+      if (c.kind != OPK_VM || m.dim() == 0) continue;
+      if (p->leaves.size() + p->tabs.size() >= static_cast<size_t>(kMaxLeaves)) break;
+      if (off + m.num_elements() > kTabBudget) break;
+      const int leaf = static_cast<int>(p->leaves.size() + p->tabs.size());
+      Plan::TabOperand tab;
+      tab.name = m.name;
+      tab.op = static_cast<int>(p->ops.size());
+      tab.count = m.num_elements();
+      tab.offset = off;
+      p->tabs.push_back(std::move(tab));
+      off += (m.num_elements() + 1) / 2 * 2;  // 16-byte aligned runs
+      p->ops.push_back(c);
+      ArrayMeta tm = m;
+      tm.name = "tabulated " + m.name;
+      tm.dtype = Dtype::float64;
+      p->tab_leaves.push_back(LeafInfo{tm, ST_F64});
+      OperandStatic plain{};
+      plain.kind = OPK_PLAIN;
+      plain.leaf = leaf;
+      plain.ndim = m.dim();
+      for (int r = 0; r < skeleton.b(); ++r)
+        for (int k = 0; k < skeleton.n(); ++k)
+          if (skeleton.args[r][k].name == m.name) p->ops[static_cast<size_t>(r) * skeleton.n() + k] = plain;
+    }
+  }
   finish_plan(*p, opt);
   return p;
 }
 
 void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream) {
+  const void* all_in[kMaxLeaves];
+  const size_t nl = plan.leaves.size(), nt = plan.tabs.size();
+  if (nt) {
+    for (size_t i = 0; i < nl; ++i) all_in[i] = d_in[i];
+    for (size_t k = 0; k < nt; ++k) all_in[nl + k] = plan.d_tab + plan.tabs[k].offset;
+    d_in = all_in;
+  }
   GenericLaunch g = plan.gen;
-  for (size_t i = 0; i < plan.leaves.size(); ++i) {
+  for (size_t i = 0; i < nl + nt; ++i) {
     g.leaves.ptr[i] = d_in[i];
-    g.leaves.storage[i] = plan.leaves[i].storage;
+    g.leaves.storage[i] = leaf_info(plan, static_cast<int>(i)).storage;
   }
   for (int r = 0; r < plan.skel.b(); ++r) g.out[r] = d_out[r];
   if (!plan.chains.empty() && !plan.coef_static)
     cuda_check(launch_coef(g.chains, g.n_chains, g.leaves, plan.d_coef, stream), "coefficient kernel");
+  for (const Plan::TabOperand& tab : plan.tabs) {
+    if (tab.kernel) {
+      TabArgs args{};
+      for (size_t k = 0; k < tab.leaf_slots.size(); ++k) args.leaf[k] = g.leaves.ptr[tab.leaf_slots[k]];
+      args.out = plan.d_tab + tab.offset;
+      args.count = tab.count;
+      cuda_check(launch_tab_kernel(tab.kernel, args, plan.sm_count, stream), "generated tabulation kernel");
+      continue;
+    }
+    TabulateLaunch t{};
+    t.op = plan.gen.ops + tab.op;
+    t.prog = plan.gen.prog;
+    t.reads = plan.gen.reads;
+    t.chains = plan.gen.chains;
+    t.n_chains = plan.gen.n_chains;
+    t.coef = plan.d_coef;
+    const ArrayMeta& m = plan.tab_leaves[static_cast<size_t>(&tab - plan.tabs.data())].meta;
+    t.ndim = m.dim();
+    for (int d = 0; d < m.dim(); ++d) t.shape[d] = m.shape[d];
+    t.first = 0;
+    t.count = tab.count;
+    t.complex_mode = false;
+    t.leaves = g.leaves;
+    t.out = plan.d_tab + tab.offset;
+    t.real_out = true;
+    cuda_check(launch_tabulate(t, stream), "tabulate kernel");
+  }
 
   if (plan.family == Family::fem_grad) {
     const FemBinding& f = plan.fem;
@@ -1422,6 +1523,8 @@ void tabulate(const Plan& plan, const std::string& name, const void* const* d_in
   if (row < 0) throw error(errc::domain, "no operand named " + name);
   TabulateLaunch t{};
   t.op = plan.gen.ops + (static_cast<size_t>(row) * e.n() + slot);
+  for (const Plan::TabOperand& tab : plan.tabs)
+    if (tab.name == name) t.op = plan.gen.ops + tab.op;  // the VM original, not its table
   t.prog = plan.gen.prog;
   t.reads = plan.gen.reads;
   t.chains = plan.gen.chains;
@@ -1477,7 +1580,16 @@ std::string describe(const Plan& p) {
       break;
     case Family::generic: launches += 1; break;
   }
+  launches += static_cast<int>(p.tabs.size());
   v.set("launches", Value::num(launches));
+  Value tabs = Value::arr();
+  Value gens = Value::arr();
+  for (const auto& t : p.tabs) {
+    tabs.push(Value::str(t.name));
+    gens.push(Value::str(t.codegen));
+  }
+  v.set("tabulated", std::move(tabs));
+  v.set("tab_codegen", std::move(gens));
   Value leaves = Value::arr();
   for (const auto& L : p.leaves) {
     Value x = feinsum::transport::meta_to_json(L.meta);

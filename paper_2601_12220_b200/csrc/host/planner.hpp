@@ -47,6 +47,7 @@ struct PlanOptions {
   bool skip_range_check = false;
   bool dry_run = false;       // plan without touching the device (CPU tests)
   std::string meta_override;  // tuner: run these parameters instead of the fact's
+  bool codegen = true;        // NVRTC tabulation kernels for VM operands (false: device VM)
 };
 
 PlanOptions parse_options(const std::string& json);
@@ -124,6 +125,24 @@ struct Plan {
   std::vector<CoefChain> chains;
   bool complex_mode = false;
 
+  // VM operands of a real-valued functional plan are tabulated at the start of
+  // every execute into plan buffers (the reference's materialize, on the
+  // device, bit-identical values) and read as plain f64 leaves, so the tuned
+  // families take them too. Synthetic leaf k has index leaves.size() + k; its
+  // program is the VM original kept at ops[op]. Empty when the plan runs the
+  // generic kernel (which evaluates the programs in place).
+  struct TabOperand {
+    std::string name;  // skeleton operand
+    int op;            // index of the VM original in ops (past the b * n slots)
+    std::int64_t count, offset;  // elements, offset in d_tab (doubles)
+    void* kernel = nullptr;       // NVRTC-compiled tabulation kernel (codegen.cpp), or the VM
+    std::vector<int> leaf_slots;  // its leaf slots -> plan leaf indices
+    std::string codegen;          // "nvrtc" | "vm: <why>"
+  };
+  std::vector<TabOperand> tabs;
+  std::vector<LeafInfo> tab_leaves;
+  double* d_tab = nullptr;
+
   // ---- normal form and retrieval ----
   bool has_canon = false;
   CanonResult canon;
@@ -153,6 +172,22 @@ struct Plan {
 
   ~Plan();
 };
+
+// Generated tabulation kernels (codegen.cpp).
+constexpr int kTabLeaves = 16;
+struct TabArgs {
+  const void* leaf[kTabLeaves];
+  double* out;
+  long long count;
+};
+std::string tab_kernel_source(const Plan& p, const OperandStatic& op, const ArrayMeta& meta,
+                              std::vector<int>* leaf_slots);
+void* compile_tab_kernel(const std::string& src, std::string* log);
+bool nvrtc_compiles(const std::string& src, std::string* log);
+int launch_tab_kernel(void* kernel, const TabArgs& args, int sm_count, void* stream);
+
+// Leaf i of the plan: a caller input, or (i >= leaves.size()) a tabulated operand.
+const LeafInfo& leaf_info(const Plan& p, int i);
 
 std::unique_ptr<Plan> make_plan(const BatchedEinsum& e, const PlanOptions& opt);
 std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,

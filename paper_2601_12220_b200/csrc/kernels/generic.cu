@@ -51,7 +51,7 @@ struct GenericEval {
     const std::int64_t* stride = p.slot_stride + k * kMaxDims;
     if (op.kind == OPK_VM) {
       for (int d = 0; d < nd; ++d) params[d] = odo.val[pos[d]];
-      return eval_vm(op, env, params);
+      return kComplex ? eval_vm(op, env, params) : cdbl{eval_vm_real(op, env, params), 0.0};
     }
     std::int64_t off = 0;
     for (int d = 0; d < nd; ++d) off += odo.val[pos[d]] * stride[d];
@@ -185,13 +185,17 @@ __global__ void __launch_bounds__(128) tabulate_kernel(const __grid_constant__ T
     }
     cdbl v;
     if (p.op->kind == OPK_VM)
-      v = eval_vm(*p.op, env, params);
+      v = kComplex ? eval_vm(*p.op, env, params) : cdbl{eval_vm_real(*p.op, env, params), 0.0};
     else if (p.op->kind == OPK_AFFINE)
       v = eval_affine<kComplex>(*p.op, env, flat);
     else
       v = load_cplx(p.leaves.ptr[p.op->leaf], p.leaves.storage[p.op->leaf], flat);
-    p.out[2 * t] = v.re;
-    p.out[2 * t + 1] = v.im;
+    if (p.real_out) {
+      p.out[t] = v.re;
+    } else {
+      p.out[2 * t] = v.re;
+      p.out[2 * t + 1] = v.im;
+    }
   }
 }
 

@@ -153,6 +153,7 @@ struct TabulateLaunch {
   bool complex_mode;
   LeafTable leaves;
   double* out;               // interleaved complex (re, im) per point
+  bool real_out;             // or: one double (re) per point (tabulated operands)
 };
 
 int launch_tabulate(const TabulateLaunch& p, void* stream);

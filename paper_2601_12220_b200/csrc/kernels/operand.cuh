@@ -184,4 +184,40 @@ __device__ inline cdbl eval_vm(const OperandStatic& op, const OperandEnv& env, c
   return cdbl{rr[0], ri[0]};
 }
 
+// The same VM on real values, for plans without complex data or sqrt: with
+// zero imaginary parts every complex step above reduces to the real operation
+// on the real parts (cmul: a*c - 0*0, cdiv: a/c, csin/ccos/cexp: the real
+// functions), so for finite values the results are bit-identical at half the
+// registers and arithmetic.
+__device__ inline double eval_vm_real(const OperandStatic& op, const OperandEnv& env, const std::int64_t* params) {
+  double rr[kMaxVmRegs];
+  for (int pc = op.prog_off; pc < op.prog_off + op.prog_len; ++pc) {
+    const VmInstr in = env.prog[pc];
+    const double a = rr[in.a & (kMaxVmRegs - 1)], b = rr[in.b & (kMaxVmRegs - 1)];
+    double v = 0.0;
+    switch (in.code) {
+      case VM_LIT: v = in.imm; break;
+      case VM_PARAM: v = static_cast<double>(params[in.arg]); break;
+      case VM_READ: {
+        const VmRead& rd = env.reads[in.arg];
+        std::int64_t off = 0;
+        for (int d = 0; d < rd.ndim; ++d) off += params[rd.param_of[d]] * rd.stride[d];
+        v = load_real(env.leaves->ptr[rd.leaf], env.leaves->storage[rd.leaf], off);
+        break;
+      }
+      case VM_ADD: v = __dadd_rn(a, b); break;
+      case VM_SUB: v = __dsub_rn(a, b); break;
+      case VM_MUL: v = __dmul_rn(a, b); break;
+      case VM_DIV: v = __ddiv_rn(a, b); break;
+      case VM_SIN: v = sin(a); break;
+      case VM_COS: v = cos(a); break;
+      case VM_EXP: v = exp(a); break;
+      case VM_SQRT: v = sqrt(a); break;  // not reached: sqrt makes the plan complex
+      case VM_RECIP: v = __ddiv_rn(1.0, a); break;
+    }
+    rr[in.dst & (kMaxVmRegs - 1)] = v;
+  }
+  return rr[0];
+}
+
 }  // namespace feb200

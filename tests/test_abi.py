@@ -62,3 +62,22 @@ def test_cpp_dropin_gpu(fe):
     exe = _build_dropin()
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_vm_operands_planned_as_tables(fe):
+    """Planning only (no device): a real-valued non-affine operand is planned
+    as a tabulated leaf feeding the tuned family; a complex one (sqrt) and a
+    plan with no tuned family keep the in-place VM on the generic kernel."""
+    from paper_2601_12220_b200 import configs as C
+    p = fe.Plan(kernel=C.wave_kernel_nonlinear(E=2_000), options={"dry_run": True})
+    assert p.info["transform"] == "fem_grad/v1" and len(p.info["tabulated"]) == 3
+    assert len(p.info["inputs"]) == 2 + 2 * 3  # caller inputs only
+    assert p.info["tab_codegen"] == ["nvrtc"] * 3  # the generated kernels compile for sm_100a
+    fk = ("domain: i<6 j<3\n"
+          "def f(p) := sqrt(X[p]) * reciprocal(Y[p])\n"
+          "array: X float64 6\narray: Y float64 6\narray: W float64 6x3\n"
+          "stmt y[j] = sum([i], f(i)*W[i,j])\n")
+    p = fe.Plan(kernel=fk, options={"dry_run": True, "storage": "wide"})
+    assert p.info["transform"] == "generic/v1" and p.info["tabulated"] == []
+    p = fe.Plan(kernel=fk.replace("sqrt(X[p])", "exp(X[p])"), options={"dry_run": True})
+    assert p.info["transform"] == "generic/v1" and p.info["tabulated"] == []

@@ -206,6 +206,47 @@ def test_wave_step_c5_functional(fe, ref, torch_cuda):
     assert k1 == k2 == fe.Plan(einsum=C.fem_grad(E=4_000)).info["key"]
 
 
+def test_tabulated_vm_operands_take_tuned_kernels(fe, ref, torch_cuda):
+    """Non-affine functional operands (here u*u - sin(k)/(2+exp(u))) are
+    tabulated on the device at the start of the execute (the reference's
+    materialize, same programs) and read as plain leaves, so the tuned family
+    runs instead of the generic kernel; results agree with the reference and
+    with the generic kernel evaluating the programs in place."""
+    from paper_2601_12220_b200 import configs as C
+    fk = C.wave_kernel_nonlinear(E=2_000)
+    info, arrays, b = _kernel_bindings(ref, fk, 13)
+    plan = fe.Plan(kernel=fk)
+    assert plan.info["transform"] == "fem_grad/v1", plan.info
+    assert len(plan.info["tabulated"]) == 3
+    got = run_plan(torch_cuda, plan, b)
+    want = ref.eval_kernel(fk, arrays, b, 3, [3, 2_000, 10])
+    assert plan.info["tab_codegen"] == ["nvrtc"] * 3
+    # the generated tabulation kernels reproduce the device VM bit for bit
+    vm = fe.Plan(kernel=fk, options={"codegen": False})
+    assert vm.info["tab_codegen"] == ["vm: codegen disabled"] * 3
+    for g, v in zip(got, run_plan(torch_cuda, vm, b)):
+        assert np.array_equal(g, v)
+    gen = fe.Plan(kernel=fk, options={"transform": "generic/v1"})
+    assert gen.info["tabulated"] == []
+    got_g = run_plan(torch_cuda, gen, b)
+    for g, w, gg in zip(got, want, got_g):
+        assert rel_err(g, w) <= FP64_TOL
+        assert rel_err(gg, w) <= FP64_TOL
+    # tensor train with a transcendental core: tt kernel over the table
+    fk = ("domain: n<64 i<64 j<64 k<64 l<64\n"
+          "def g(a,c) := exp(H[a,c] / 4)\n"
+          "def h(a,c) := K[a,c]\n"
+          "def x(m,a,c) := X[m,a,c]\n"
+          "array: H float64 64x64\narray: K float64 64x64\narray: X float64 64x64x64\n"
+          "stmt y[n,i,k] = sum([j,l], g(i,j)*h(k,l)*x(n,j,l))\n")
+    info, arrays, b = _kernel_bindings(ref, fk, 17)
+    plan = fe.Plan(kernel=fk)
+    assert plan.info["transform"] == "tt/v1" and len(plan.info["tabulated"]) == 1, plan.info
+    got = run_plan(torch_cuda, plan, b)
+    want = ref.eval_kernel(fk, arrays, b, 1, [64, 64, 64])
+    assert rel_err(got[0], want[0]) <= FP64_TOL
+
+
 def test_squared_kernel_vm(fe, ref, torch_cuda, fixtures):
     """Transcendental functional operands run in the device VM."""
     fk = fixtures["squared_kernel.fk"]

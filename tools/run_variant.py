@@ -1,6 +1,7 @@
 """Run one config with forced kernel parameters (for ncu captures / A-B runs).
 
   python tools/run_variant.py C5 "mma=1;stages=4" [reps]
+  python tools/run_variant.py C5-nonlinear generic     # force the generic kernel
 """
 import os
 import sys
@@ -17,9 +18,16 @@ from paper_2601_12220_b200 import feinsum as fe  # noqa: E402
 def main():
     name, meta = sys.argv[1], sys.argv[2]
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-    kind, payload = bench.spec(name)
+    if name == "C5-nonlinear":
+        from paper_2601_12220_b200 import configs as C
+        kind, payload = "kernel", C.wave_kernel_nonlinear()
+    else:
+        kind, payload = bench.spec(name)
     base = fe.Plan(einsum=payload) if kind == "einsum" else fe.Plan(kernel=payload)
-    opts = {"meta": meta, "transform": base.info["transform"]} if meta else {}
+    if meta == "generic":
+        opts = {"transform": "generic/v1"}
+    else:
+        opts = {"meta": meta, "transform": base.info["transform"]} if meta else {}
     plan = fe.Plan(einsum=payload, options=opts) if kind == "einsum" else fe.Plan(kernel=payload, options=opts)
     ins = []
     for k, m in enumerate(plan.inputs):

@@ -91,7 +91,9 @@ int fe_retrieve(const char* path, const char* key, const char* device, char** ou
  *      evaluate_functional, raising.hpp:58) ---- */
 
 /* options JSON (all optional): {"storage": "native"|"wide", "leaf_storage": {name: "f64"|...},
- *  "facts": path, "device": "b200", "transform": "generic/v1"|...} */
+ *  "facts": path, "device": "b200", "transform": "generic/v1"|..., "meta": "k=v;...",
+ *  "codegen": true|false (NVRTC tabulation kernels for non-affine operands; false: device VM),
+ *  "dry_run": true (plan on the host only)} */
 int fe_plan_create(const char* einsum_json, const char* options_json, fe_plan_t* out);
 /* .fk kernel text: inputs = declared arrays in name order, one output per stmt */
 int fe_plan_create_kernel(const char* fk_text, const char* options_json, fe_plan_t* out);

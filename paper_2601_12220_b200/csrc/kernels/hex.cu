@@ -393,6 +393,33 @@ __device__ __forceinline__ void pass_c(double* io) {
     for (int n = 0; n < Q; ++n) io[m * Q + n] = v[m][n];
 }
 
+// pass C with the direction sum fused (one warp per (direction, plane), the
+// plane's three direction warps chained by named barriers): x = 0 stores its
+// partial into the staging tile, x = 1 adds its own after x = 0's arrive, x =
+// 2 after x = 1's — (p0 + p1) + p2, the order the separate sum pass used, so
+// the output is unchanged. No partials in W, no extra pass, no CTA barrier.
+// Chain barriers b0 (x = 0 -> 1) and b0 + 1 (x = 1 -> 2); every lane of the
+// warp takes part (bar is warp-aligned), lanes without a task compute on
+// zeros and store nothing.
+template <int Q, int X>
+__device__ __forceinline__ void pass_c_sum(const double* in, double* ys, int b0, bool active) {
+  double v[Q][Q];
+#pragma unroll
+  for (int b = 0; b < Q; ++b)
+#pragma unroll
+    for (int c = 0; c < Q; ++c) v[b][c] = active ? in[b * Q + c] : 0.0;
+  cols_c<Q, 4, X, true>(v);
+  rows_c<Q, 5, X, true>(v);
+  if constexpr (X > 0) asm volatile("bar.sync %0, 64;" ::"r"(b0 + X - 1) : "memory");
+  if (active) {
+#pragma unroll
+    for (int m = 0; m < Q; ++m)
+#pragma unroll
+      for (int n = 0; n < Q; ++n) ys[m * Q + n] = X == 0 ? v[m][n] : ys[m * Q + n] + v[m][n];
+  }
+  if constexpr (X < 2) asm volatile("bar.arrive %0, 64;" ::"r"(b0 + X) : "memory");
+}
+
 // F1[y] along j on one line (y compile-time)
 template <int Q, int Y>
 __device__ __forceinline__ void line_f1(double (&t)[Q]) {
@@ -530,6 +557,8 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
   // pass B: thread -> (line, element, field pair (f, f + H)), line fastest
   const int H = (R + 1) / 2;
   const int nbt = H * NE * Q2;
+  // every warp of pass C one (direction, plane): fuse the direction sum
+  const bool fused = nblk == 32 && Q <= 7;
 
   int it = 0;
   for (std::int64_t st = blockIdx.x; st < nstages; st += gridDim.x, ++it) {
@@ -557,18 +586,33 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
       double* const wl[2] = {w0, f1 < R ? W + (f1 * NE + el) * CS + kl : w0};
       pass_b<Q, 2>(wl, ds, g, NE * Q3);
     }
+    if (producer) ptx::bulk_wait_read<0>();  // the previous stage's stores have read Ys
     __syncthreads();
     if (producer && more) issue_g(st + gridDim.x);
 
+    const std::int64_t e0 = st * NE;
+    if (fused) {
+      if (pactive) {
+        double* ys = Ys + pcube * Q3 + pplane * Q2;  // cube * Q3 = field * NE * Q3 + element * Q3
+        if (dir == 0) pass_c_sum<Q, 0>(a_out, ys, 1 + 2 * pplane, true);
+        else if (dir == 1) pass_c_sum<Q, 1>(a_out, ys, 1 + 2 * pplane, true);
+        else pass_c_sum<Q, 2>(a_out, ys, 1 + 2 * pplane, true);
+      }
+      ptx::fence_proxy_async();
+      __syncthreads();  // W is rewritten by the next stage's pass A; Ys complete
+      if (producer) {
+        for (int f = 0; f < R; ++f) ptx::bulk_s2g(p.Y[f] + e0 * Q3, Ys + f * NE * Q3, bytes);
+        ptx::bulk_commit();
+      }
+      continue;
+    }
     if (pactive) {
       if (dir == 0) pass_c<Q, 0>(a_out);
       else if (dir == 1) pass_c<Q, 1>(a_out);
       else pass_c<Q, 2>(a_out);
     }
-    if (producer) ptx::bulk_wait_read<0>();  // the previous stage's stores have read Ys
     __syncthreads();
 
-    const std::int64_t e0 = st * NE;
     // sum the three direction partials into the staging tile (a field's
     // stage output is one contiguous run of NE * Q3 doubles), then one bulk
     // copy per field streams it to HBM while the next stage computes —

@@ -590,7 +590,8 @@ bool gett_operand(const Plan& p, const OperandStatic& op, int* leaf, int* alpha,
   } else {
     return false;
   }
-  return leaf_info(p, *leaf).storage == ST_F64;
+  const int st = leaf_info(p, *leaf).storage;
+  return st == ST_F64 || st == ST_F32;
 }
 
 // GETT family: 2 slots, pure contraction (every index in exactly two of A, B,
@@ -664,6 +665,41 @@ bool bind_gett(Plan& p, std::string* why) {
   GettBinding g;
   g.pack_a = !a_ok;
   g.pack_b = !b_ok;
+  // storage: uniform per role over the rows (f64 or f32); fp32 operands are
+  // widened through the pack pass
+  {
+    const int n = c.n();
+    int a_st = -1, b_st = -1, c_st = -1;
+    for (int q = 0; q < c.b(); ++q) {
+      const int ur = p.canon.sigma_row[q];
+      const OperandStatic& oa = p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[sa]];
+      const OperandStatic& ob = p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[sb]];
+      const int la_leaf = oa.kind == OPK_AFFINE ? oa.term[0].leaf : oa.leaf;
+      const int lb_leaf = ob.kind == OPK_AFFINE ? ob.term[0].leaf : ob.leaf;
+      if (la_leaf < 0 || lb_leaf < 0 || (oa.kind != OPK_PLAIN && oa.kind != OPK_AFFINE) ||
+          (ob.kind != OPK_PLAIN && ob.kind != OPK_AFFINE)) {
+        *why = "operands are not plain or alpha*X+beta";
+        return false;
+      }
+      const int sa_ = leaf_info(p, la_leaf).storage, sb_ = leaf_info(p, lb_leaf).storage, sc_ = p.outputs[ur].storage;
+      if ((a_st >= 0 && sa_ != a_st) || (b_st >= 0 && sb_ != b_st) || (c_st >= 0 && sc_ != c_st)) {
+        *why = "mixed storage across rows";
+        return false;
+      }
+      a_st = sa_;
+      b_st = sb_;
+      c_st = sc_;
+    }
+    if ((a_st != ST_F64 && a_st != ST_F32) || (b_st != ST_F64 && b_st != ST_F32) || (c_st != ST_F64 && c_st != ST_F32)) {
+      *why = "storage other than f64 / f32";
+      return false;
+    }
+    g.a_f32 = a_st == ST_F32;
+    g.b_f32 = b_st == ST_F32;
+    g.c_f32 = c_st == ST_F32;
+    g.pack_a = g.pack_a || g.a_f32;
+    g.pack_b = g.pack_b || g.b_f32;
+  }
   g.ext_mo = lens.at(mo);
   g.ext_mi = lens.at(mi);
   g.ext_no = lens.at(no);
@@ -717,7 +753,7 @@ bool bind_gett(Plan& p, std::string* why) {
   g.c_no = stride_of(c.i_out, shc, no);
   g.c_ni = stride_of(c.i_out, shc, ni);
   g.role_names = "mo=" + mo + " mi=" + mi + " no=" + no + " ni=" + ni + " kA=" + ka + " kB=" + kb +
-                 (g.pack_a ? " packA" : "") + (g.pack_b ? " packB" : "");
+                 (g.pack_a ? " packA" : "") + (g.pack_b ? " packB" : "") + (g.a_f32 || g.b_f32 || g.c_f32 ? " f32io" : "");
   const int n = c.n();
   for (int q = 0; q < c.b(); ++q) {
     const int ur = p.canon.sigma_row[q];
@@ -725,11 +761,7 @@ bool bind_gett(Plan& p, std::string* why) {
     r.out_row = ur;
     if (!gett_operand(p, p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[sa]], &r.a_leaf, &r.a_alpha, &r.a_beta) ||
         !gett_operand(p, p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[sb]], &r.b_leaf, &r.b_alpha, &r.b_beta)) {
-      *why = "operands are not plain or alpha*X+beta f64";
-      return false;
-    }
-    if (p.outputs[ur].storage != ST_F64) {
-      *why = "non-f64 output";
+      *why = "operands are not plain or alpha*X+beta f64 / f32";
       return false;
     }
     g.rows.push_back(r);
@@ -1197,6 +1229,10 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
       cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_pack_b),
                             sizeof(double) * static_cast<size_t>(g.ext_no * g.ext_ni * g.ext_ka * g.ext_kb)),
                  "cudaMalloc(gett packed B)");
+    if (g.c_f32)
+      cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_cbuf),
+                            sizeof(double) * static_cast<size_t>(g.ext_mo * g.ext_mi * g.ext_no * g.ext_ni)),
+                 "cudaMalloc(gett f64 result)");
   }
 }
 
@@ -1215,6 +1251,7 @@ Plan::~Plan() {
   if (d_scratch) cudaFree(d_scratch);
   if (d_pack_a) cudaFree(d_pack_a);
   if (d_pack_b) cudaFree(d_pack_b);
+  if (d_cbuf) cudaFree(d_cbuf);
   if (d_tab) cudaFree(d_tab);
 }
 
@@ -1430,15 +1467,19 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         L.B = static_cast<const double*>(d_in[r.b_leaf]);
         if (b.pack_a) {
           const std::int64_t ext[4] = {b.ext_mo, b.ext_mi, b.ext_kb, b.ext_ka};
-          cuda_check(permute4(L.A, plan.d_pack_a, ext, b.a_src, stream), "gett pack A");
+          cuda_check(b.a_f32 ? permute4_widen(static_cast<const float*>(d_in[r.a_leaf]), plan.d_pack_a, ext, b.a_src, stream)
+                             : permute4(L.A, plan.d_pack_a, ext, b.a_src, stream),
+                     "gett pack A");
           L.A = plan.d_pack_a;
         }
         if (b.pack_b) {
           const std::int64_t ext[4] = {b.ext_no, b.ext_ni, b.ext_ka, b.ext_kb};
-          cuda_check(permute4(L.B, plan.d_pack_b, ext, b.b_src, stream), "gett pack B");
+          cuda_check(b.b_f32 ? permute4_widen(static_cast<const float*>(d_in[r.b_leaf]), plan.d_pack_b, ext, b.b_src, stream)
+                             : permute4(L.B, plan.d_pack_b, ext, b.b_src, stream),
+                     "gett pack B");
           L.B = plan.d_pack_b;
         }
-        L.C = static_cast<double*>(d_out[r.out_row]);
+        L.C = b.c_f32 ? plan.d_cbuf : static_cast<double*>(d_out[r.out_row]);
         L.a_alpha = r.a_alpha;
         L.a_beta = r.a_beta;
         L.b_alpha = r.b_alpha;
@@ -1449,6 +1490,10 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         L.group = meta_int(plan.meta, "group", 12);
         L.grid = meta_int(plan.meta, "grid", 0);
         cuda_check(launch_gett(L, stream), "gett kernel");
+        if (b.c_f32)
+          cuda_check(narrow_f64_f32(plan.d_cbuf, static_cast<float*>(d_out[r.out_row]),
+                                    b.ext_mo * b.ext_mi * b.ext_no * b.ext_ni, stream),
+                     "gett narrow C");
       }
       return;
     }
@@ -1574,7 +1619,7 @@ std::string describe(const Plan& p) {
     case Family::tt: launches += static_cast<int>(p.tt.rows.size()); break;
     case Family::gett:
       for (const auto& r : p.gett.rows) {
-        launches += 1 + (p.gett.pack_a ? 1 : 0) + (p.gett.pack_b ? 1 : 0);
+        launches += 1 + (p.gett.pack_a ? 1 : 0) + (p.gett.pack_b ? 1 : 0) + (p.gett.c_f32 ? 1 : 0);
         if (r.a_alpha >= 0 || r.b_alpha >= 0) launches += 2;
       }
       break;

@@ -84,6 +84,10 @@ struct GettBinding {
   // per execute into a plan buffer laid out [mo][mi][kB][kA] (A) or
   // [no][ni][kA][kB] (B); *_src are the source strides in that dim order
   bool pack_a = false, pack_b = false;
+  // fp32 operands are widened into the pack buffers (the reference computes
+  // float32 in double, so the f64 DMMA path is its arithmetic); an fp32
+  // output is accumulated in d_cbuf and narrowed once
+  bool a_f32 = false, b_f32 = false, c_f32 = false;
   std::int64_t a_src[4] = {0, 0, 0, 0}, b_src[4] = {0, 0, 0, 0};
   struct Row {
     int a_leaf, b_leaf, out_row;
@@ -167,6 +171,7 @@ struct Plan {
   double* d_scratch = nullptr;  // family workspace (GETT affine K-sums)
   double* d_pack_a = nullptr;   // GETT repacked operands (see GettBinding)
   double* d_pack_b = nullptr;
+  double* d_cbuf = nullptr;     // GETT f64 result staging for fp32 outputs
   GenericLaunch gen{};  // pointers filled per execution
   int sm_count = 148;
 

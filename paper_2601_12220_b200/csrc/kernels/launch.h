@@ -265,6 +265,9 @@ int flush_l2(void* scratch, std::int64_t bytes, void* stream);
 // repacks a strided operand into a kernel's layout (GETT operands whose
 // unit-stride index is not a contracted one)
 int permute4(const double* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream);
+// the same from an fp32 source, widened to fp64; and a dense fp64 -> fp32 copy
+int permute4_widen(const float* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream);
+int narrow_f64_f32(const double* src, float* dst, std::int64_t n, void* stream);
 // which: 0 = DFMA (CUDA cores), 1 = DMMA m8n8k4 (FP64 tensor cores)
 int fp64_peak(int which, double* tflops);
 

@@ -135,15 +135,18 @@ int fill_dyadic(void* ptr, int storage, std::int64_t count, std::uint64_t seed, 
 // 4-D permute through a 32 x 32 shared tile over (dst inner dim, src unit-
 // stride dim) so both the reads and the writes are coalesced; the other two
 // dims ride on blockIdx.z. When the src's unit-stride dim is the dst's inner
-// dim (or none is unit stride) it is a plain strided copy.
+// dim (or none is unit stride) it is a plain strided copy. The source may be
+// fp32 (widened on the way: fp32 operands of the f64 DMMA GETT).
+template <typename T>
 struct Permute4 {
-  const double* src;
+  const T* src;
   double* dst;
   std::int64_t ext[4], ss[4], ds[4];
   int u;  // dst dim whose src stride is 1 (-1: none)
 };
 
-__global__ void permute4_tiled(const __grid_constant__ Permute4 p) {
+template <typename T>
+__global__ void permute4_tiled(const __grid_constant__ Permute4<T> p) {
   __shared__ double tile[32][33];
   // dims: 3 = dst inner (x tile), u = src inner (y tile), the other two (a, b) on z
   const int u = p.u;
@@ -158,7 +161,7 @@ __global__ void permute4_tiled(const __grid_constant__ Permute4 p) {
   // read: consecutive threads walk the src unit-stride dim u
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const std::int64_t x = x0 + r, y = y0 + threadIdx.x;
-    if (x < p.ext[3] && y < p.ext[u]) tile[r][threadIdx.x] = __ldg(p.src + base_s + x * p.ss[3] + y);
+    if (x < p.ext[3] && y < p.ext[u]) tile[r][threadIdx.x] = static_cast<double>(__ldg(p.src + base_s + x * p.ss[3] + y));
   }
   __syncthreads();
   // write: consecutive threads walk the dst inner dim 3
@@ -168,7 +171,8 @@ __global__ void permute4_tiled(const __grid_constant__ Permute4 p) {
   }
 }
 
-__global__ void permute4_plain(const __grid_constant__ Permute4 p) {
+template <typename T>
+__global__ void permute4_plain(const __grid_constant__ Permute4<T> p) {
   const std::int64_t n = p.ext[0] * p.ext[1] * p.ext[2] * p.ext[3];
   for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
@@ -178,12 +182,27 @@ __global__ void permute4_plain(const __grid_constant__ Permute4 p) {
       r /= p.ext[d];
       off += i * p.ss[d];
     }
-    p.dst[t] = __ldg(p.src + off);
+    p.dst[t] = static_cast<double>(__ldg(p.src + off));
   }
 }
 
-int permute4(const double* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream) {
-  Permute4 p{};
+// dense copies: widen fp32 -> fp64 or narrow fp64 -> fp32, 4 values per thread
+template <typename S, typename D>
+__global__ void convert_kernel(const S* __restrict__ src, D* __restrict__ dst, std::int64_t n) {
+  const std::int64_t n4 = n / 4;
+  for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < n4;
+       t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[4 * t + k] = static_cast<D>(__ldg(src + 4 * t + k));
+  }
+  for (std::int64_t t = 4 * n4 + blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    dst[t] = static_cast<D>(__ldg(src + t));
+}
+
+template <typename T>
+int permute4_t(const T* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream) {
+  Permute4<T> p{};
   p.src = src;
   p.dst = dst;
   p.u = -1;
@@ -203,12 +222,33 @@ int permute4(const double* src, double* dst, const std::int64_t ext[4], const st
       if (d != p.u) (oa < 0 ? oa : ob) = d;
     const dim3 grid(static_cast<unsigned>((ext[3] + 31) / 32), static_cast<unsigned>((ext[p.u] + 31) / 32),
                     static_cast<unsigned>(ext[oa] * ext[ob]));
-    permute4_tiled<<<grid, dim3(32, 8), 0, st>>>(p);
+    permute4_tiled<T><<<grid, dim3(32, 8), 0, st>>>(p);
   } else {
     int sms = 148;
     device_sm_count(&sms);
-    permute4_plain<<<sms * 8, 256, 0, st>>>(p);
+    bool dense = true;
+    for (int d = 0; d < 4; ++d) dense = dense && (ext[d] == 1 || p.ss[d] == p.ds[d]);
+    if (dense)
+      convert_kernel<T, double><<<sms * 8, 256, 0, st>>>(src, dst, acc);
+    else
+      permute4_plain<T><<<sms * 8, 256, 0, st>>>(p);
   }
+  return cudaGetLastError();
+}
+
+int permute4(const double* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream) {
+  return permute4_t<double>(src, dst, ext, src_stride, stream);
+}
+
+int permute4_widen(const float* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream) {
+  return permute4_t<float>(src, dst, ext, src_stride, stream);
+}
+
+int narrow_f64_f32(const double* src, float* dst, std::int64_t n, void* stream) {
+  if (n == 0) return cudaSuccess;
+  int sms = 148;
+  device_sm_count(&sms);
+  convert_kernel<double, float><<<sms * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
   return cudaGetLastError();
 }
 

@@ -278,6 +278,29 @@ def _tccg_small(ref, fe, a_ext=2, c_ext=2, e_ext=8, f_ext=8):
             "args": [[am("A", [lens[s] for s in "aebf"]), am("B", [lens[s] for s in "dfce"])]]}
 
 
+def test_gett_fp32_operands_widened(fe, ref, torch_cuda):
+    """float32 TCCG operands run on the f64 DMMA GETT (widened in the pack pass,
+    as the reference computes float32 in double); an fp32 output is narrowed
+    once at the end. Dyadic inputs: exact sums, so the result equals the
+    reference's double value rounded to float32 — bitwise. Mixed f32 / f64
+    operands (f64 output) are exact too."""
+    for dts, dims in [(("float32", "float32"), (2, 2, 8, 8)), (("float32", "float32"), (3, 1, 8, 16)),
+                      (("float32", "float64"), (2, 2, 8, 8)), (("float64", "float32"), (1, 2, 16, 8))]:
+        e = _tccg_small(ref, fe, *dims)
+        for k, dt in enumerate(dts):
+            e["args"][0][k]["dtype"] = dt
+        plan = fe.Plan(einsum=e)
+        assert plan.info["transform"] == "gett_dmma/v1", plan.info
+        b = ref.random_bindings(e, sum(dims) + 5)
+        got = run_plan(torch_cuda, plan, b)
+        want = ref.evaluate(e, b)[0].real
+        if dts == ("float32", "float32"):
+            assert got[0].dtype == np.float32
+            assert np.array_equal(got[0], want.astype(np.float32)), dims
+        else:
+            assert np.array_equal(got[0], want), dims
+
+
 def test_gett_dmma_bit_exact_small(fe, ref, torch_cuda):
     """TCCG abcd-aebf-dfce through the TMA+DMMA kernel: dyadic inputs make
     every partial sum exact, so the result must equal the reference bitwise."""

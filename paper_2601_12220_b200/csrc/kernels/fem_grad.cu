@@ -38,12 +38,21 @@ struct Coef {
 // per SM (more warps in flight for the HBM-bound loop); chosen per fact meta.
 // EPT: elements per consumer thread (el, el + TE/EPT, ...): more independent
 // FMA chains per thread and D reused from registers across them.
+// Consumer threads: TE * NI / EPT, padded to whole warps (tiles such as
+// TE = 34 / 68 that make E = 1e4 exactly one tile per CTA slot leave a few
+// padding threads idle).
+template <int NX, int NR, int NI, int NJ, int TE, int EPT>
+constexpr int fem_consumers() {
+  return (TE * NI / EPT + 31) / 32 * 32;
+}
+
 template <int NX, int NR, int NI, int NJ, int TE, bool kPlainU, bool kDSmem, int EPT = 1>
-__global__ void __launch_bounds__(32 + TE * NI / EPT, kDSmem ? 2 : 1)
+__global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(), kDSmem ? 2 : 1)
     fem_grad_kernel(const __grid_constant__ FemGradLaunch p) {
-  constexpr int kConsumers = TE * NI / EPT;
+  constexpr int kConsumers = fem_consumers<NX, NR, NI, NJ, TE, EPT>();
+  constexpr int kWorkers = TE * NI / EPT;  // consumers with an (element, i) task
   constexpr int kES = TE / EPT;  // element stride between a thread's elements
-  static_assert(kConsumers % 32 == 0, "consumer threads must fill warps");
+  static_assert(TE % EPT == 0 && TE % 2 == 0, "tile shape");
   constexpr int kConsumerWarps = kConsumers / 32;
   static_assert(NJ % 2 == 0, "U rows are read as double2");
   constexpr int kUTile = TE * NJ;          // doubles per U tile
@@ -197,7 +206,7 @@ __global__ void __launch_bounds__(32 + TE * NI / EPT, kDSmem ? 2 : 1)
       urow_stride = kUTile;
     }
 
-    if (e0 + el < E) {
+    if (c < kWorkers && e0 + el < E) {
       for (int q = 0; q < p.rows; ++q) {
         const double* dq_row = dsm + p.row_d[q] * NX * NI * NJ + i * NJ;  // D_q[x][i][:] at x*NI*NJ
         if (!kDSmem && p.row_d[q] != cur_d) {
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(32 + TE * NI / EPT, kDSmem ? 2 : 1)
 
 template <int NX, int NR, int NI, int NJ, int TE, int EPT = 1>
 int launch_shape(const FemGradLaunch& p, cudaStream_t s) {
-  constexpr int kThreads = 32 + TE * NI / EPT;
+  constexpr int kThreads = 32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>();
   const bool plain = p.plain_u;
   const size_t doubles = static_cast<size_t>(p.n_d) * NX * NI * NJ +
                          static_cast<size_t>(p.stages) * (p.n_j * NX * NR * TE + p.n_u * TE * NJ) +
@@ -307,6 +316,9 @@ int launch_fem_grad(const FemGradLaunch& p, void* stream) {
     if (p.ept == 2) {
       // 64-element tiles: one tile per SM for small batches (C1: 157 tiles)
       if (p.tile_e == 64) return launch_shape<3, 3, 10, 10, 64, 2>(p, s);
+      // one tile per CTA slot at C1's E = 1e4: 148 x 68 / 296 x 34 elements
+      if (p.tile_e == 68) return launch_shape<3, 3, 10, 10, 68, 2>(p, s);
+      if (p.tile_e == 34) return launch_shape<3, 3, 10, 10, 34, 2>(p, s);
       return launch_shape<3, 3, 10, 10, 32, 2>(p, s);
     }
     return launch_shape<3, 3, 10, 10, 32>(p, s);

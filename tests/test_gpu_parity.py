@@ -149,7 +149,7 @@ def test_fem_grad_odd_sizes(fe, ref, torch_cuda):
         assert np.array_equal(g, w.real)
 
 
-FEM_VARIANTS = ["stages=2", "stages=4;te=16", "stages=3;dsmem=1", "stages=4;ept=2", "stages=2;ept=2;te=64", "mma=1;stages=4", "mma=1;stages=2;te=16",
+FEM_VARIANTS = ["stages=2", "stages=4;te=16", "stages=3;dsmem=1", "stages=4;ept=2", "stages=2;ept=2;te=64", "stages=4;ept=2;te=34", "stages=3;ept=2;te=68", "mma=1;stages=4", "mma=1;stages=2;te=16",
                 "mma=1;stages=3;te=64"]
 
 

@@ -511,6 +511,7 @@ bool bind_fem(Plan& p, std::string* why) {
   }
   const int n = p.skel.n();
   int u_tiles = 0;
+  int elem_st = -1;
   for (int q = 0; q < f.rows; ++q) {
     const int ur = p.canon.sigma_row[q];
     auto operand = [&](int role) -> const OperandStatic& {
@@ -523,8 +524,14 @@ bool bind_fem(Plan& p, std::string* why) {
       *why = "functional J or D operand";
       return false;
     }
-    if (leaf_info(p, J.leaf).storage != ST_F64 || leaf_info(p, D.leaf).storage != ST_F64) {
-      *why = "non-f64 storage";
+    // one element type for every array of the plan: f64, or f32 (the fp32
+    // kernel instance; E % 4 == 0 so its bulk-copy rows stay 16-byte aligned)
+    auto same_storage = [&](int st) {
+      if (elem_st < 0) elem_st = st;
+      return st == elem_st && (st == ST_F64 || (st == ST_F32 && f.E % 4 == 0));
+    };
+    if (!same_storage(leaf_info(p, J.leaf).storage) || !same_storage(leaf_info(p, D.leaf).storage)) {
+      *why = "storage other than uniform f64 / f32 (f32: E % 4 == 0)";
       return false;
     }
     std::vector<AffineTerm> terms;
@@ -543,8 +550,8 @@ bool bind_fem(Plan& p, std::string* why) {
       return false;
     }
     for (const auto& t : terms)
-      if (leaf_info(p, t.leaf).storage != ST_F64) {
-        *why = "non-f64 storage";
+      if (!same_storage(leaf_info(p, t.leaf).storage)) {
+        *why = "storage other than uniform f64 / f32 (f32: E % 4 == 0)";
         return false;
       }
     u_tiles += static_cast<int>(terms.size());
@@ -552,11 +559,12 @@ bool bind_fem(Plan& p, std::string* why) {
     f.d_leaf.push_back(D.leaf);
     f.u_terms.push_back(std::move(terms));
     f.out_row.push_back(ur);
-    if (p.outputs[ur].storage != ST_F64) {
-      *why = "non-f64 output";
+    if (!same_storage(p.outputs[ur].storage)) {
+      *why = "output storage differs from the inputs'";
       return false;
     }
   }
+  f.f32 = elem_st == ST_F32;
   if (u_tiles > kFemMaxUTiles) {
     *why = "too many U tiles";
     return false;
@@ -1431,7 +1439,8 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
     L.tile_e = meta_int(plan.meta, "te", f.NI == 10 ? 32 : (f.NI == 4 ? 64 : 16));
     L.grid = meta_int(plan.meta, "grid", 0);  // 0: all resident CTAs
     L.ept = meta_int(plan.meta, "ept", 1);
-    L.mma = meta_int(plan.meta, "mma", 0) != 0 && fem_mma_supported(L.NX, L.NR, L.NI, L.NJ);
+    L.f32 = f.f32;
+    L.mma = !f.f32 && meta_int(plan.meta, "mma", 0) != 0 && fem_mma_supported(L.NX, L.NR, L.NI, L.NJ);
     if (ok) {
       if (L.mma)
         cuda_check(launch_fem_mma(L, stream), "fem_mma kernel");

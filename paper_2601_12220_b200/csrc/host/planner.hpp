@@ -72,6 +72,7 @@ struct FemBinding {
   // per canonical row: leaf indices / output row
   std::vector<int> j_leaf, d_leaf, out_row;
   std::vector<std::vector<AffineTerm>> u_terms;  // per row; leaf indices
+  bool f32 = false;  // every array float32 (fp32 kernel instance)
 };
 
 // Roles of the GETT family (dense 2-operand contraction on DMMA).

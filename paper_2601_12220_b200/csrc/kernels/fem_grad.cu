@@ -33,6 +33,27 @@ struct Coef {
   int sign;
 };
 
+// element type: fp64 (C1 / C5) or fp32 (float32 einsums of the same shape;
+// the same kernel with half the bytes per element)
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double2 mk2(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, b); }
+
 // kDSmem: read D from shared memory (broadcast LDS.128) instead of holding
 // D[x,i,:] in 60 registers — halves the register footprint so two CTAs fit
 // per SM (more warps in flight for the HBM-bound loop); chosen per fact meta.
@@ -46,9 +67,11 @@ constexpr int fem_consumers() {
   return (TE * NI / EPT + 31) / 32 * 32;
 }
 
-template <int NX, int NR, int NI, int NJ, int TE, bool kPlainU, bool kDSmem, int EPT = 1>
+template <typename T, int NX, int NR, int NI, int NJ, int TE, bool kPlainU, bool kDSmem, int EPT = 1>
 __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(), kDSmem ? 2 : 1)
     fem_grad_kernel(const __grid_constant__ FemGradLaunch p) {
+  using V2 = typename Vec2<T>::type;
+  static_assert(TE * sizeof(T) % 16 == 0, "bulk-copy rows are 16-byte multiples");
   constexpr int kConsumers = fem_consumers<NX, NR, NI, NJ, TE, EPT>();
   constexpr int kWorkers = TE * NI / EPT;  // consumers with an (element, i) task
   constexpr int kES = TE / EPT;  // element stride between a thread's elements
@@ -61,10 +84,11 @@ __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(),
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int S = p.stages;
   const int stage_doubles = p.n_j * kJTile + p.n_u * kUTile;
-  double* dsm = reinterpret_cast<double*>(smem_raw);                   // D copies
-  double* ring = dsm + p.n_d * NX * NI * NJ;                            // stages
-  double* ucomb = ring + static_cast<size_t>(S) * stage_doubles;        // [2][rows][TE*NJ]
-  Coef* coefs = reinterpret_cast<Coef*>(ucomb + (kPlainU ? 0 : 2 * p.rows * kUTile));
+  T* dsm = reinterpret_cast<T*>(smem_raw);                         // D copies
+  T* ring = dsm + p.n_d * NX * NI * NJ;                            // stages
+  T* ucomb = ring + static_cast<size_t>(S) * stage_doubles;        // [2][rows][TE*NJ]
+  Coef* coefs = reinterpret_cast<Coef*>(
+      (reinterpret_cast<std::uintptr_t>(ucomb + (kPlainU ? 0 : 2 * p.rows * kUTile)) + 15) & ~std::uintptr_t{15});
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(coefs + kFemMaxUTiles);
   std::uint64_t* empty = full + S;
 
@@ -77,16 +101,17 @@ __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(),
   auto issue = [&](std::int64_t tile, int s) {
     const std::int64_t e0 = tile * TE;
     const int cnt = static_cast<int>(E - e0 < TE ? E - e0 : TE);
-    const std::uint32_t jb = static_cast<std::uint32_t>(cnt) * 8u;
-    const std::uint32_t ub = static_cast<std::uint32_t>(cnt) * NJ * 8u;
+    const std::uint32_t jb = static_cast<std::uint32_t>(cnt * sizeof(T));
+    const std::uint32_t ub = static_cast<std::uint32_t>(cnt * NJ * sizeof(T));
     ptx::mbar_arrive_expect_tx(&full[s], static_cast<std::uint32_t>(p.n_j * NX * NR) * jb +
                                              static_cast<std::uint32_t>(p.n_u) * ub);
-    double* st = ring + static_cast<size_t>(s) * stage_doubles;
+    T* st = ring + static_cast<size_t>(s) * stage_doubles;
     for (int a = 0; a < p.n_j; ++a)
       for (int xr = 0; xr < NX * NR; ++xr)
-        ptx::bulk_g2s_hint(st + a * kJTile + xr * TE, p.J[a] + xr * E + e0, jb, &full[s], pol);
-    double* su = st + p.n_j * kJTile;
-    for (int u = 0; u < p.n_u; ++u) ptx::bulk_g2s_hint(su + u * kUTile, p.U[u] + e0 * NJ, ub, &full[s], pol);
+        ptx::bulk_g2s_hint(st + a * kJTile + xr * TE, reinterpret_cast<const T*>(p.J[a]) + xr * E + e0, jb, &full[s], pol);
+    T* su = st + p.n_j * kJTile;
+    for (int u = 0; u < p.n_u; ++u)
+      ptx::bulk_g2s_hint(su + u * kUTile, reinterpret_cast<const T*>(p.U[u]) + e0 * NJ, ub, &full[s], pol);
   };
   // the producer thread starts the first S tile loads before the CTA-wide
   // setup below, so their latency overlaps it (matters for small E, e.g. C1)
@@ -105,12 +130,12 @@ __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(),
     // round trip in the prologue instead of one per loop trip)
     constexpr int kPer = 4;
     const int nd = p.n_d * NX * NI * NJ;
-    double v[kPer];
+    T v[kPer];
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const int t = tid + k * static_cast<int>(blockDim.x);
       const int which = t / (NX * NI * NJ);
-      v[k] = t < nd ? __ldg(p.D[which] + (t - which * NX * NI * NJ)) : 0.0;
+      v[k] = t < nd ? __ldg(reinterpret_cast<const T*>(p.D[which]) + (t - which * NX * NI * NJ)) : T(0);
     }
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
@@ -119,7 +144,7 @@ __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(),
     }
     for (int t = tid + kPer * static_cast<int>(blockDim.x); t < nd; t += blockDim.x) {
       const int which = t / (NX * NI * NJ);
-      dsm[t] = __ldg(p.D[which] + (t - which * NX * NI * NJ));
+      dsm[t] = __ldg(reinterpret_cast<const T*>(p.D[which]) + (t - which * NX * NI * NJ));
     }
   }
   if (!kPlainU && tid < p.n_u) {
@@ -149,7 +174,7 @@ __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(),
   const int c = tid - 32;
   const int el = c / NI;
   const int i = c - el * NI;
-  double dreg[kDSmem ? 1 : NX][kDSmem ? 2 : NJ];
+  T dreg[kDSmem ? 1 : NX][kDSmem ? 2 : NJ];
   int cur_d = -1;
   int it = 0;
   for (std::int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -157,45 +182,43 @@ __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(),
     const std::uint32_t round = static_cast<std::uint32_t>(it / S);
     ptx::mbar_wait(&full[s], round & 1u);
     const std::int64_t e0 = tile * TE;
-    const double* st = ring + static_cast<size_t>(s) * stage_doubles;
-    const double* su = st + p.n_j * kJTile;
+    const T* st = ring + static_cast<size_t>(s) * stage_doubles;
+    const T* su = st + p.n_j * kJTile;
 
     // K2 prologue: combine every row's U leaves once per tile
-    const double* ubase;
+    const T* ubase;
     int urow_stride;
     if (kPlainU) {
       ubase = su;
       urow_stride = kUTile;  // row q reads leaf tile row_u_first[q] == q
     } else {
-      double* uc = ucomb + (it & 1) * p.rows * kUTile;
+      T* uc = ucomb + (it & 1) * p.rows * kUTile;
       // (pre * leaf) * post per term, terms accumulated left to right — the
       // operand's own order; two values per thread and iteration (16-byte
       // shared accesses), the two-term form a*x +- b*y with its coefficients
       // in registers
-      auto term = [](const Coef& cf, double v) { return __dmul_rn(__dmul_rn(cf.pre, v), cf.post); };
-      auto join = [](const Coef& cf, double acc, double x) {
-        return cf.sign > 0 ? __dadd_rn(acc, x) : __dsub_rn(acc, x);
-      };
+      auto term = [](const Coef& cf, T v) { return mul_rn(mul_rn(static_cast<T>(cf.pre), v), static_cast<T>(cf.post)); };
+      auto join = [](const Coef& cf, T acc, T x) { return cf.sign > 0 ? add_rn(acc, x) : sub_rn(acc, x); };
       for (int q = 0; q < p.rows; ++q) {
         const int u0 = p.row_u_first[q], nt = p.row_u_count[q];
-        const double2* s0 = reinterpret_cast<const double2*>(su + u0 * kUTile);
-        double2* o = reinterpret_cast<double2*>(uc + q * kUTile);
+        const V2* s0 = reinterpret_cast<const V2*>(su + u0 * kUTile);
+        V2* o = reinterpret_cast<V2*>(uc + q * kUTile);
         if (nt == 2) {
           const Coef c0 = coefs[u0], c1 = coefs[u0 + 1];
-          const double2* s1 = s0 + kUTile / 2;
+          const V2* s1 = s0 + kUTile / 2;
           for (int v = c; v < kUTile / 2; v += kConsumers) {
-            const double2 a = s0[v], b = s1[v];
-            o[v] = make_double2(join(c1, term(c0, a.x), term(c1, b.x)), join(c1, term(c0, a.y), term(c1, b.y)));
+            const V2 a = s0[v], b = s1[v];
+            o[v] = mk2(join(c1, term(c0, a.x), term(c1, b.x)), join(c1, term(c0, a.y), term(c1, b.y)));
           }
         } else {
           for (int v = c; v < kUTile / 2; v += kConsumers) {
             const Coef c0 = coefs[u0];
-            const double2 a = s0[v];
-            double2 acc = make_double2(term(c0, a.x), term(c0, a.y));
+            const V2 a = s0[v];
+            V2 acc = mk2(term(c0, a.x), term(c0, a.y));
             for (int k = 1; k < nt; ++k) {
               const Coef ck = coefs[u0 + k];
-              const double2 b = s0[k * (kUTile / 2) + v];
-              acc = make_double2(join(ck, acc.x, term(ck, b.x)), join(ck, acc.y, term(ck, b.y)));
+              const V2 b = s0[k * (kUTile / 2) + v];
+              acc = mk2(join(ck, acc.x, term(ck, b.x)), join(ck, acc.y, term(ck, b.y)));
             }
             o[v] = acc;
           }
@@ -208,32 +231,32 @@ __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(),
 
     if (c < kWorkers && e0 + el < E) {
       for (int q = 0; q < p.rows; ++q) {
-        const double* dq_row = dsm + p.row_d[q] * NX * NI * NJ + i * NJ;  // D_q[x][i][:] at x*NI*NJ
+        const T* dq_row = dsm + p.row_d[q] * NX * NI * NJ + i * NJ;  // D_q[x][i][:] at x*NI*NJ
         if (!kDSmem && p.row_d[q] != cur_d) {
           cur_d = p.row_d[q];
-          const double* dq = dsm + cur_d * NX * NI * NJ;
+          const T* dq = dsm + cur_d * NX * NI * NJ;
 #pragma unroll
           for (int x = 0; x < NX; ++x)
 #pragma unroll
             for (int j = 0; j < NJ; ++j) dreg[x][j] = dq[(x * NI + i) * NJ + j];
         }
         (void)dq_row;
-        const double* ur = ubase + (kPlainU ? p.row_u_first[q] : q) * urow_stride + el * NJ;
-        double t[EPT][NX];
+        const T* ur = ubase + (kPlainU ? p.row_u_first[q] : q) * urow_stride + el * NJ;
+        T t[EPT][NX];
 #pragma unroll
         for (int h = 0; h < EPT; ++h)
 #pragma unroll
-          for (int x = 0; x < NX; ++x) t[h][x] = 0.0;
+          for (int x = 0; x < NX; ++x) t[h][x] = T(0);
 #pragma unroll
         for (int j = 0; j < NJ; j += 2) {
-          double2 u[EPT];
+          V2 u[EPT];
 #pragma unroll
-          for (int h = 0; h < EPT; ++h) u[h] = *reinterpret_cast<const double2*>(ur + h * kES * NJ + j);
+          for (int h = 0; h < EPT; ++h) u[h] = *reinterpret_cast<const V2*>(ur + h * kES * NJ + j);
 #pragma unroll
           for (int x = 0; x < NX; ++x) {
-            double d0, d1;
+            T d0, d1;
             if constexpr (kDSmem) {
-              const double2 dd = *reinterpret_cast<const double2*>(dq_row + x * NI * NJ + j);
+              const V2 dd = *reinterpret_cast<const V2*>(dq_row + x * NI * NJ + j);
               d0 = dd.x;
               d1 = dd.y;
             } else {
@@ -247,13 +270,13 @@ __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(),
             }
           }
         }
-        const double* jt = st + p.row_j[q] * kJTile;
-        double* yq = p.Y[q];
+        const T* jt = st + p.row_j[q] * kJTile;
+        T* yq = reinterpret_cast<T*>(p.Y[q]);
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
 #pragma unroll
           for (int h = 0; h < EPT; ++h) {
-            double y = 0.0;
+            T y = T(0);
 #pragma unroll
             for (int x = 0; x < NX; ++x) y = fma(jt[(x * NR + r) * TE + el + h * kES], t[h][x], y);
             if (h == 0 || e0 + el + h * kES < E)
@@ -267,14 +290,14 @@ __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(),
   }
 }
 
-template <int NX, int NR, int NI, int NJ, int TE, int EPT = 1>
+template <typename T, int NX, int NR, int NI, int NJ, int TE, int EPT = 1>
 int launch_shape(const FemGradLaunch& p, cudaStream_t s) {
   constexpr int kThreads = 32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>();
   const bool plain = p.plain_u;
   const size_t doubles = static_cast<size_t>(p.n_d) * NX * NI * NJ +
                          static_cast<size_t>(p.stages) * (p.n_j * NX * NR * TE + p.n_u * TE * NJ) +
                          (plain ? 0 : 2 * static_cast<size_t>(p.rows) * TE * NJ);
-  const size_t smem = sizeof(double) * doubles + sizeof(Coef) * kFemMaxUTiles + sizeof(std::uint64_t) * 2 * p.stages;
+  const size_t smem = sizeof(T) * doubles + 16 + sizeof(Coef) * kFemMaxUTiles + sizeof(std::uint64_t) * 2 * p.stages;
   auto run = [&](auto kern) -> int {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -289,15 +312,15 @@ int launch_shape(const FemGradLaunch& p, cudaStream_t s) {
     return cudaGetLastError();
   };
   if constexpr (EPT > 1) {
-    if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, false, EPT>);
-    return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, false, EPT>);
+    if (plain) return run(fem_grad_kernel<T, NX, NR, NI, NJ, TE, true, false, EPT>);
+    return run(fem_grad_kernel<T, NX, NR, NI, NJ, TE, false, false, EPT>);
   } else {
     if (p.d_in_smem) {
-      if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, true>);
-      return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, true>);
+      if (plain) return run(fem_grad_kernel<T, NX, NR, NI, NJ, TE, true, true>);
+      return run(fem_grad_kernel<T, NX, NR, NI, NJ, TE, false, true>);
     }
-    if (plain) return run(fem_grad_kernel<NX, NR, NI, NJ, TE, true, false>);
-    return run(fem_grad_kernel<NX, NR, NI, NJ, TE, false, false>);
+    if (plain) return run(fem_grad_kernel<T, NX, NR, NI, NJ, TE, true, false>);
+    return run(fem_grad_kernel<T, NX, NR, NI, NJ, TE, false, false>);
   }
 }
 
@@ -307,25 +330,31 @@ bool fem_grad_supported(int NX, int NR, int NI, int NJ) {
   return NX == 3 && NR == 3 && ((NI == 10 && NJ == 10) || (NI == 4 && NJ == 4) || (NI == 20 && NJ == 20));
 }
 
+template <typename T>
+int launch_fem_grad_t(const FemGradLaunch& p, cudaStream_t s) {
+  if (p.NI == 10 && p.NJ == 10) {
+    // small batches: half-size tiles put more CTAs in flight (latency-bound)
+    if (p.tile_e == 16) return launch_shape<T, 3, 3, 10, 10, 16>(p, s);
+    if (p.ept == 2) {
+      // 64-element tiles: one tile per SM for small batches (C1: 157 tiles)
+      if (p.tile_e == 64) return launch_shape<T, 3, 3, 10, 10, 64, 2>(p, s);
+      // one tile per CTA slot at C1's E = 1e4: 148 x 68 / 296 x 34 elements
+      if (p.tile_e == 68) return launch_shape<T, 3, 3, 10, 10, 68, 2>(p, s);
+      if constexpr (sizeof(T) == 8)  // fp32 rows of 34 are not 16-byte multiples
+        if (p.tile_e == 34) return launch_shape<T, 3, 3, 10, 10, 34, 2>(p, s);
+      return launch_shape<T, 3, 3, 10, 10, 32, 2>(p, s);
+    }
+    return launch_shape<T, 3, 3, 10, 10, 32>(p, s);
+  }
+  if (p.NI == 4 && p.NJ == 4) return launch_shape<T, 3, 3, 4, 4, 64>(p, s);
+  if (p.NI == 20 && p.NJ == 20) return launch_shape<T, 3, 3, 20, 20, 16>(p, s);
+  return cudaErrorInvalidValue;
+}
+
 int launch_fem_grad(const FemGradLaunch& p, void* stream) {
   if (p.E == 0) return cudaSuccess;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (p.NI == 10 && p.NJ == 10) {
-    // small batches: half-size tiles put more CTAs in flight (latency-bound)
-    if (p.tile_e == 16) return launch_shape<3, 3, 10, 10, 16>(p, s);
-    if (p.ept == 2) {
-      // 64-element tiles: one tile per SM for small batches (C1: 157 tiles)
-      if (p.tile_e == 64) return launch_shape<3, 3, 10, 10, 64, 2>(p, s);
-      // one tile per CTA slot at C1's E = 1e4: 148 x 68 / 296 x 34 elements
-      if (p.tile_e == 68) return launch_shape<3, 3, 10, 10, 68, 2>(p, s);
-      if (p.tile_e == 34) return launch_shape<3, 3, 10, 10, 34, 2>(p, s);
-      return launch_shape<3, 3, 10, 10, 32, 2>(p, s);
-    }
-    return launch_shape<3, 3, 10, 10, 32>(p, s);
-  }
-  if (p.NI == 4 && p.NJ == 4) return launch_shape<3, 3, 4, 4, 64>(p, s);
-  if (p.NI == 20 && p.NJ == 20) return launch_shape<3, 3, 20, 20, 16>(p, s);
-  return cudaErrorInvalidValue;
+  return p.f32 ? launch_fem_grad_t<float>(p, s) : launch_fem_grad_t<double>(p, s);
 }
 
 }  // namespace feb200

@@ -183,6 +183,7 @@ struct FemGradLaunch {
   bool d_in_smem;      // D read from shared memory (2 CTAs/SM) instead of registers
   bool mma;            // fem_mma.cu: inner contraction on DMMA (fp64 tensor cores)
   int ept;             // elements per consumer thread (1 or 2)
+  bool f32;            // J, D, U, Y are float (pointers reinterpreted); E % 4 == 0
   const double* coef;  // interleaved complex coefficients (real part used)
   double* Y[kFemMaxRows];
 };

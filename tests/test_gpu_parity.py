@@ -175,6 +175,30 @@ def test_fem_grad_variants(fe, ref, torch_cuda, meta):
         assert rel_err(g, w) <= FP64_TOL, meta
 
 
+@pytest.mark.parametrize("meta", ["", "stages=4", "stages=3;dsmem=1", "stages=2;ept=2;te=64", "stages=4;te=16"])
+def test_fem_grad_fp32(fe, ref, torch_cuda, meta):
+    """float32 arrays take the fp32 instance of K1 (same kernel, half the
+    bytes): within the fp32 bar of the reference (which computes in double),
+    plain and functional (u + 0.5 k) operands, ragged tails."""
+    from paper_2601_12220_b200 import configs as C
+    opts = {"meta": meta, "transform": "fem_grad/v1"} if meta else None
+    for E, nb in [(4, 1), (1_004, 3), (10_000, 3)]:
+        e = C.fem_grad(E=E, b=nb, dtype="float32")
+        plan = fe.Plan(einsum=e, options=opts) if opts else fe.Plan(einsum=e)
+        assert plan.info["transform"] == "fem_grad/v1", plan.info
+        assert plan.outputs[0]["storage"] == "f32"
+        bind = ref.random_bindings(e, E + 3)
+        for g, w in zip(run_plan(torch_cuda, plan, bind), ref.evaluate(e, bind)):
+            assert g.dtype == np.float32 and rel_err(g, w.real) <= 1e-5, (meta, E)
+    fk = C.wave_kernel(E=4_000).replace("float64", "float32")
+    info, arrays, b = _kernel_bindings(ref, fk, 19)
+    plan = fe.Plan(kernel=fk, options=opts) if opts else fe.Plan(kernel=fk)
+    assert plan.info["transform"] == "fem_grad/v1"
+    want = ref.eval_kernel(fk, arrays, b, 3, [3, 4_000, 10])
+    for g, w in zip(run_plan(torch_cuda, plan, b), want):
+        assert rel_err(g, w) <= 1e-5, meta
+
+
 def _kernel_bindings(ref, fk, seed):
     info = ref.raise_kernel(fk)
     import re

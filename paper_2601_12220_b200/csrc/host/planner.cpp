@@ -1729,7 +1729,7 @@ std::unique_ptr<Plan> make_shard(const Plan& full, int rank, int world, const Pl
   // fem_grad moves elements in pairs (16-byte bulk-copy runs); hex in stages
   // of four when the axis allows it (the four-element kernel), else pairs
   std::int64_t unit = 1;
-  if (full.family == Family::fem_grad) unit = 2;
+  if (full.family == Family::fem_grad) unit = full.fem.f32 ? 4 : 2;  // fp32: 16-byte bulk-copy rows
   if (full.family == Family::hex) unit = lens.at(ix) % 4 == 0 ? 4 : 2;
   const std::int64_t units = n / unit;
   std::int64_t a = units * rank / world * unit, b = units * (rank + 1) / world * unit;

@@ -33,6 +33,7 @@ def _worker(rank, world, port, results):
         "C3": dict(kernel=C.tccg_kernel(a_ext=144)),
         "C4": dict(einsum=C.tensor_train(n=8192)),
         "C5": dict(kernel=C.wave_kernel(E=40_000)),
+        "C1-f32": dict(einsum=C.fem_grad(E=20_004, dtype="float32")),  # fp32: shards in fours
         "generic": dict(einsum={"i_out": ["i", "j"], "i_in": [["i", "k"], ["k", "j"]],
                                 "args": [[{"name": "A", "shape": [6, 3], "dtype": "float64"},
                                           {"name": "B", "shape": [3, 5], "dtype": "float64"}]]}),
@@ -65,7 +66,7 @@ def test_shards_tile_the_axis_gloo():
         assert len({p[2] for p in parts}) == 1, name  # one axis
         for p in parts:
             assert p[3] == p[4], name  # the shard runs the global plan's transform
-        if name == "C2":  # hex shards keep the four-element stage of the kernel
+        if name in ("C2", "C1-f32"):  # hex stages of four; fp32 FEM 16-byte rows
             assert all(p[0] % 4 == 0 for p in parts), parts
         if name != "generic":
             # replicated operand prologues (C3's shared opB) may add a little

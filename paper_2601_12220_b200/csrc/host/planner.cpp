@@ -602,10 +602,236 @@ bool gett_operand(const Plan& p, const OperandStatic& op, int* leaf, int* alpha,
   return st == ST_F64 || st == ST_F32;
 }
 
-// GETT family: 2 slots, pure contraction (every index in exactly two of A, B,
-// C), 2+2+2 indices, C's unit-stride index on the B side, A's and B's
-// unit-stride indices both contracted.
+// Storage of the GETT roles over all rows (uniform f64 or f32 per role) and
+// the operand rows; shared by both binders below.
+bool gett_rows(Plan& p, GettBinding& g, int sa, int sb, std::string* why) {
+  const BatchedEinsum& c = p.canon.canonical;
+  const int n = c.n();
+  int a_st = -1, b_st = -1, c_st = -1;
+  for (int q = 0; q < c.b(); ++q) {
+    const int ur = p.canon.sigma_row[q];
+    GettBinding::Row r{};
+    r.out_row = ur;
+    if (!gett_operand(p, p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[sa]], &r.a_leaf, &r.a_alpha, &r.a_beta) ||
+        !gett_operand(p, p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[sb]], &r.b_leaf, &r.b_alpha, &r.b_beta)) {
+      *why = "operands are not plain or alpha*X+beta f64 / f32";
+      return false;
+    }
+    const int sa_ = leaf_info(p, r.a_leaf).storage, sb_ = leaf_info(p, r.b_leaf).storage, sc_ = p.outputs[ur].storage;
+    if ((a_st >= 0 && sa_ != a_st) || (b_st >= 0 && sb_ != b_st) || (c_st >= 0 && sc_ != c_st)) {
+      *why = "mixed storage across rows";
+      return false;
+    }
+    a_st = sa_;
+    b_st = sb_;
+    c_st = sc_;
+    g.rows.push_back(r);
+  }
+  if (c_st != ST_F64 && c_st != ST_F32) {
+    *why = "output storage other than f64 / f32";
+    return false;
+  }
+  g.a_f32 = a_st == ST_F32;
+  g.b_f32 = b_st == ST_F32;
+  g.c_f32 = c_st == ST_F32;
+  return true;
+}
+
+// GETT over index groups of one or two indices (matmul-shaped contractions:
+// `ab,bc->ac`, `abc,cd->abd`, ...). A group of two indices maps onto the
+// kernel's (outer, inner) dims as in bind_gett; a group of one index x of
+// extent L is reshaped into (L / s, s) — offsets x * sigma = (x / s) * (s *
+// sigma) + (x % s) * sigma, so no data moves. M / N inner extents must fit a
+// 72-row box (24..72), K parts must be even; operands whose unit-stride dim is
+// not the kernel's (A: kA, B: kB) are repacked per execute as in bind_gett.
+bool bind_gett_split(Plan& p, std::string* why) {
+  const BatchedEinsum& c = p.canon.canonical;
+  if (p.complex_mode || c.n() != 2) {
+    *why = "not a 2-operand contraction";
+    return false;
+  }
+  const feinsum::IndexList &l0 = c.i_in[0], &l1 = c.i_in[1];
+  const std::set<std::string> s0(l0.begin(), l0.end()), s1(l1.begin(), l1.end()), so(c.i_out.begin(), c.i_out.end());
+  if (s0.size() != l0.size() || s1.size() != l1.size() || so.size() != c.i_out.size()) {
+    *why = "repeated indices";
+    return false;
+  }
+  std::vector<std::string> K, M0, N1;  // K in operand 0's order
+  for (const auto& x : l0) {
+    const bool in1 = s1.count(x) > 0, ino = so.count(x) > 0;
+    if (in1 && ino) {
+      *why = "batch index";
+      return false;
+    }
+    if (!in1 && !ino) {
+      *why = "index summed within one operand";
+      return false;
+    }
+    (in1 ? K : M0).push_back(x);
+  }
+  for (const auto& x : l1) {
+    if (s0.count(x)) continue;
+    if (!so.count(x)) {
+      *why = "index summed within one operand";
+      return false;
+    }
+    N1.push_back(x);
+  }
+  if (K.empty() || M0.empty() || N1.empty() || K.size() > 2 || M0.size() > 2 || N1.size() > 2) {
+    *why = "index groups of one or two indices only";
+    return false;
+  }
+  const auto lens = feinsum::index_lengths(c);
+  auto strides = [&](const feinsum::IndexList& l, const std::vector<std::int64_t>& shape) {
+    std::map<std::string, std::int64_t> m;
+    const auto st = row_major_strides(shape);
+    for (size_t d = 0; d < l.size(); ++d) m[l[d]] = st[d];
+    return m;
+  };
+  std::vector<std::int64_t> shc;
+  for (const auto& x : c.i_out) shc.push_back(lens.at(x));
+  const auto st0 = strides(l0, c.args[0][0].shape), st1 = strides(l1, c.args[0][1].shape), stc = strides(c.i_out, shc);
+  // operand roles: B is the operand holding C's unit-stride index (coalesced
+  // C stores run along the kernel's ni)
+  const bool swap = std::find(M0.begin(), M0.end(), c.i_out.back()) != M0.end();
+  const int sa = swap ? 1 : 0, sb = 1 - sa;
+  const auto& stA = swap ? st1 : st0;
+  const auto& stB = swap ? st0 : st1;
+  const std::vector<std::string>& M = swap ? N1 : M0;
+  const std::vector<std::string>& N = swap ? M0 : N1;
+  struct VD {
+    std::int64_t ext = 1, a = 0, b = 0, c = 0;  // extent, strides in A, B, C
+  };
+  auto vd_of = [&](const std::string& x) {
+    VD v;
+    v.ext = lens.at(x);
+    v.a = stA.count(x) ? stA.at(x) : 0;
+    v.b = stB.count(x) ? stB.at(x) : 0;
+    v.c = stc.count(x) ? stc.at(x) : 0;
+    return v;
+  };
+  auto split = [](const VD& v, std::int64_t inner, VD* outer, VD* in) {
+    *in = v;
+    in->ext = inner;
+    *outer = v;
+    outer->ext = v.ext / inner;
+    outer->a = v.a * inner;
+    outer->b = v.b * inner;
+    outer->c = v.c * inner;
+  };
+  // (outer, inner) of an M / N group: inner extent in 24..72 (largest divisor)
+  auto mn_dims = [&](const std::vector<std::string>& grp, bool by_c, VD* outer, VD* in) {
+    if (grp.size() == 2) {
+      VD x = vd_of(grp[0]), y = vd_of(grp[1]);
+      const bool y_inner = by_c ? y.c < x.c : (M == grp ? y.a < x.a : y.b < x.b);
+      *in = y_inner ? y : x;
+      *outer = y_inner ? x : y;
+      if (!(in->ext >= 24 && in->ext <= 72) && outer->ext >= 24 && outer->ext <= 72) std::swap(*in, *outer);
+      return in->ext >= 24 && in->ext <= 72;
+    }
+    const VD v = vd_of(grp[0]);
+    for (std::int64_t d = 72; d >= 24; --d)
+      if (v.ext % d == 0) {
+        split(v, d, outer, in);
+        return true;
+      }
+    return false;
+  };
+  VD mo, mi, no, ni, ka, kb;
+  if (!mn_dims(M, false, &mo, &mi) || !mn_dims(N, true, &no, &ni)) {
+    *why = "M / N extents have no 24..72 inner part";
+    return false;
+  }
+  if (K.size() == 2) {
+    VD x = vd_of(K[0]), y = vd_of(K[1]);
+    // kA = A's finer-stride K index
+    ka = x.a < y.a ? x : y;
+    kb = x.a < y.a ? y : x;
+  } else {
+    // one K index: kA (A's part) inner, kB outer; both even, kA a multiple
+    // of the 8-wide A box where possible
+    const VD v = vd_of(K[0]);
+    std::int64_t best = 0;
+    for (std::int64_t d : {8, 16, 32, 64, 4, 2, 24, 40, 48, 56, 12, 20, 28, 36, 44, 6, 10, 14, 18, 22, 26, 30})
+      if (v.ext % d == 0 && (v.ext / d) % 2 == 0) {
+        best = d;
+        break;
+      }
+    if (!best) {
+      *why = "K extent has no even x even split";
+      return false;
+    }
+    split(v, best, &kb, &ka);
+  }
+  GettBinding g;
+  g.ext_mo = mo.ext;
+  g.ext_mi = mi.ext;
+  g.ext_no = no.ext;
+  g.ext_ni = ni.ext;
+  g.ext_ka = ka.ext;
+  g.ext_kb = kb.ext;
+  if (!gett_supported(g.ext_mi, g.ext_ni, g.ext_ka, g.ext_kb)) {
+    *why = "extents outside the kernel box (mi, ni in 24..72, even K extents)";
+    return false;
+  }
+  if (!gett_rows(p, g, sa, sb, why)) return false;
+  // A: kA unit stride, other strides even (16-byte TMA strides); B: kB
+  g.pack_a = g.a_f32 || ka.a != 1 || mo.a % 2 || mi.a % 2 || kb.a % 2;
+  g.pack_b = g.b_f32 || kb.b != 1 || no.b % 2 || ni.b % 2 || ka.b % 2;
+  if (g.pack_a) {
+    const std::int64_t src[4] = {mo.a, mi.a, kb.a, ka.a};
+    std::copy(src, src + 4, g.a_src);
+    g.a_kb = g.ext_ka;
+    g.a_mi = g.ext_kb * g.ext_ka;
+    g.a_mo = g.ext_mi * g.a_mi;
+  } else {
+    g.a_mo = mo.a;
+    g.a_mi = mi.a;
+    g.a_kb = kb.a;
+  }
+  if (g.pack_b) {
+    const std::int64_t src[4] = {no.b, ni.b, ka.b, kb.b};
+    std::copy(src, src + 4, g.b_src);
+    g.b_ka = g.ext_kb;
+    g.b_ni = g.ext_ka * g.ext_kb;
+    g.b_no = g.ext_ni * g.b_ni;
+  } else {
+    g.b_no = no.b;
+    g.b_ni = ni.b;
+    g.b_ka = ka.b;
+  }
+  g.c_mo = mo.c;
+  g.c_mi = mi.c;
+  g.c_no = no.c;
+  g.c_ni = ni.c;
+  auto names = [](const std::vector<std::string>& v) {
+    std::string r;
+    for (const auto& x : v) r += x;
+    return r;
+  };
+  g.role_names = "split M=" + names(M) + " (" + std::to_string(g.ext_mo) + "x" + std::to_string(g.ext_mi) + ") N=" +
+                 names(N) + " (" + std::to_string(g.ext_no) + "x" + std::to_string(g.ext_ni) + ") K=" + names(K) +
+                 " (" + std::to_string(g.ext_kb) + "x" + std::to_string(g.ext_ka) + ")" + (g.pack_a ? " packA" : "") +
+                 (g.pack_b ? " packB" : "") + (g.a_f32 || g.b_f32 || g.c_f32 ? " f32io" : "");
+  p.gett = std::move(g);
+  return true;
+}
+
+bool bind_gett4(Plan& p, std::string* why);
+
+// GETT family: the 2+2+2-index TCCG form (bind_gett4), else the split form.
 bool bind_gett(Plan& p, std::string* why) {
+  std::string w4;
+  if (bind_gett4(p, &w4)) return true;
+  if (bind_gett_split(p, why)) return true;
+  *why = w4 + "; " + *why;
+  return false;
+}
+
+// 2 slots, pure contraction (every index in exactly two of A, B, C), 2+2+2
+// indices, C's unit-stride index on the B side, A's and B's unit-stride
+// indices both contracted.
+bool bind_gett4(Plan& p, std::string* why) {
   const BatchedEinsum& c = p.canon.canonical;
   if (p.complex_mode || c.n() != 2 || c.i_out.size() != 4) {
     *why = "not a 2-operand 4-index contraction";

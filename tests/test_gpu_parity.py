@@ -302,6 +302,32 @@ def _tccg_small(ref, fe, a_ext=2, c_ext=2, e_ext=8, f_ext=8):
             "args": [[am("A", [lens[s] for s in "aebf"]), am("B", [lens[s] for s in "dfce"])]]}
 
 
+def test_gett_split_groups_matmul_shapes(fe, ref, torch_cuda):
+    """Contractions whose M / N / K groups have one index (matmul shapes) run
+    on the GETT kernel by reshaping the index into (outer, inner) dims; exact
+    on dyadic data like the TCCG form (float32: the reference's double value
+    rounded once)."""
+    m = lambda n, s, dt="float64": {"name": n, "shape": s, "dtype": dt}  # noqa: E731
+    cases = [
+        {"i_out": ["a", "c"], "i_in": [["a", "b"], ["b", "c"]], "args": [[m("A", [128, 256]), m("B", [256, 96])]]},
+        {"i_out": ["a", "c"], "i_in": [["b", "a"], ["c", "b"]], "args": [[m("A", [256, 120]), m("B", [72, 256])]]},
+        {"i_out": ["a", "b", "d"], "i_in": [["a", "b", "c"], ["c", "d"]], "args": [[m("A", [30, 40, 64]), m("B", [64, 48])]]},
+        {"i_out": ["d", "a"], "i_in": [["a", "c"], ["c", "d"]], "args": [[m("A", [50, 72]), m("B", [72, 144])]]},
+        {"i_out": ["a", "b"], "i_in": [["a", "c"], ["b", "c"]],
+         "args": [[m("A", [100, 128], "float32"), m("B", [96, 128], "float32")]]},
+    ]
+    for k, e in enumerate(cases):
+        plan = fe.Plan(einsum=e)
+        assert plan.info["transform"] == "gett_dmma/v1", (k, plan.info)
+        b = ref.random_bindings(e, 40 + k)
+        got = run_plan(torch_cuda, plan, b)[0]
+        want = ref.evaluate(e, b)[0].real
+        if got.dtype == np.float32:
+            assert np.array_equal(got, want.astype(np.float32)), k
+        else:
+            assert np.array_equal(got, want), k
+
+
 def test_gett_fp32_operands_widened(fe, ref, torch_cuda):
     """float32 TCCG operands run on the f64 DMMA GETT (widened in the pack pass,
     as the reference computes float32 in double); an fp32 output is narrowed

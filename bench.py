@@ -380,6 +380,8 @@ def e2e_pass(args, loads, torch, fe, world, dist, cdev=None):
     stream = torch.cuda.current_stream()
     rates, h2d, d2h, ms = [], 0, 0, 0.0
     steps = max(1, min(args.steps, 3))
+    bw = pcie_bandwidth(torch, stream)
+    per = {}
     for w in loads:
         hin = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in w.ins]
         for h, t in zip(hin, w.ins):
@@ -403,13 +405,40 @@ def e2e_pass(args, loads, torch, fe, world, dist, cdev=None):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t = tt.item()
         rates.append(w.flops * world / t / 1e9)
-        h2d += sum(x.numel() * x.element_size() for x in hin)
-        d2h += sum(x.numel() * x.element_size() for x in hout)
+        bi = sum(x.numel() * x.element_size() for x in hin)
+        bo = sum(x.numel() * x.element_size() for x in hout)
+        h2d += bi
+        d2h += bo
         ms += t * 1e3
+        # PCIe floor: both directions overlapped (the host pipeline runs H2D,
+        # kernels and D2H of different chunks on three streams)
+        floor = max(bi / bw["h2d_gbs"], bo / bw["d2h_gbs"]) / 1e9
+        per[w.name] = {"ms": t * 1e3, "gflops": w.flops * world / t / 1e9, "h2d_bytes": bi, "d2h_bytes": bo,
+                       "pcie_floor_ms": floor * 1e3, "pcie_frac": floor / t}
         del hin, hout
     return {"value": math.exp(sum(math.log(r) for r in rates) / len(rates)), "unit": "GFLOP/s",
             "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": ms,
-            "steps": steps, "path": "fe_plan_execute_host (C-ABI), pinned host buffers"}
+            "steps": steps, "path": "fe_plan_execute_host (C-ABI), pinned host buffers",
+            "pcie": bw, "per_config": per}
+
+
+def pcie_bandwidth(torch, stream, nbytes=1 << 30):
+    """Pinned host <-> device copy bandwidth (GB/s), 1 GiB each way, events."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = {}
+    for key, fn in (("h2d_gbs", lambda: d.copy_(h, non_blocking=True)), ("d2h_gbs", lambda: h.copy_(d, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(3):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out[key] = 3 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    del h, d
+    return out
 
 
 # ------------------------------------------------------ CPU reference ----

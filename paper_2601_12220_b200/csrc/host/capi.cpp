@@ -508,7 +508,8 @@ std::unique_ptr<HostPipe> make_pipe(const fe_plan_s& h) {
   if (bytes < (std::int64_t{256} << 20)) return nullptr;
   // 8 chunks (measured on the suite: 8 and 16 tie, 32 loses to per-chunk
   // launch and copy overheads); FE_PIPE_CHUNKS overrides for experiments
-  const int chunks = std::getenv("FE_PIPE_CHUNKS") ? std::max(2, std::atoi(std::getenv("FE_PIPE_CHUNKS"))) : 8;
+  const int chunks = std::getenv("FE_PIPE_CHUNKS") ? std::max(2, std::atoi(std::getenv("FE_PIPE_CHUNKS")))
+                                                  : feb200::pipe_chunks(p, 8);
   auto pipe = std::make_unique<HostPipe>();
   const feb200::PlanOptions opt = feb200::parse_options(h.options);
   try {

@@ -809,6 +809,7 @@ bool bind_gett_split(Plan& p, std::string* why) {
     for (const auto& x : v) r += x;
     return r;
   };
+  g.shard_m = M[0];
   g.role_names = "split M=" + names(M) + " (" + std::to_string(g.ext_mo) + "x" + std::to_string(g.ext_mi) + ") N=" +
                  names(N) + " (" + std::to_string(g.ext_no) + "x" + std::to_string(g.ext_ni) + ") K=" + names(K) +
                  " (" + std::to_string(g.ext_kb) + "x" + std::to_string(g.ext_ka) + ")" + (g.pack_a ? " packA" : "") +
@@ -986,6 +987,7 @@ bool bind_gett4(Plan& p, std::string* why) {
   g.c_mi = stride_of(c.i_out, shc, mi);
   g.c_no = stride_of(c.i_out, shc, no);
   g.c_ni = stride_of(c.i_out, shc, ni);
+  g.shard_m = mo;
   g.role_names = "mo=" + mo + " mi=" + mi + " no=" + no + " ni=" + ni + " kA=" + ka + " kB=" + kb +
                  (g.pack_a ? " packA" : "") + (g.pack_b ? " packB" : "") + (g.a_f32 || g.b_f32 || g.c_f32 ? " f32io" : "");
   const int n = c.n();
@@ -1931,19 +1933,38 @@ std::string shard_index_of(const Plan& p) {
     case Family::tt: return role({"ij", "kl", "njl"}, "nik", 'n');
     case Family::hex:
       return role({"xai", "xbm", "xcn", "xyeabc", "yaj", "ybk", "ycl", "ejkl"}, "eimn", 'e');
-    case Family::gett: {
-      // mo: the outer M index (first M index of the A slot)
-      const std::string names = p.gett.role_names;
-      const auto at = names.find("mo=");
-      const std::string mo = names.substr(at + 3, names.find(' ', at) - at - 3);
-      return p.canon.sigma_idx.at(mo);
-    }
+    case Family::gett:
+      // the outer M index (4-index form: mo; split form: the M group's first)
+      return p.canon.sigma_idx.at(p.gett.shard_m);
     case Family::generic: break;
   }
   return p.skel.i_out.empty() ? std::string() : p.skel.i_out[0];
 }
 
 }  // namespace
+
+int pipe_chunks(const Plan& p, int dflt) {
+  if (p.family != Family::gett || p.gett.role_names.rfind("mo=", 0) != 0) return dflt;
+  // GETT (4-index form, shards along mo): wave quantisation of each chunk's
+  // launch dominates — C3 in 8 chunks of 9 mo is 180 tiles = 2 waves on 148
+  // SMs, in 9 chunks of 8 mo 144 tiles = one. Pick the chunk count whose
+  // chunks fill whole waves best (ties: closest to the default).
+  const std::int64_t n = p.gett.ext_mo, no_tiles = (p.gett.ext_no + 1) / 2;
+  const int sms = p.sm_count > 0 ? p.sm_count : 148;
+  int best = dflt;
+  double best_score = -1.0;
+  for (int c = 3; c <= 16 && c <= n; ++c) {
+    const std::int64_t mo_c = (n + c - 1) / c;
+    const std::int64_t tiles = (mo_c + 1) / 2 * no_tiles;
+    const std::int64_t waves = (tiles + sms - 1) / sms;
+    const double score = static_cast<double>(tiles) / static_cast<double>(waves * sms) - 0.005 * std::abs(c - dflt);
+    if (score > best_score) {
+      best_score = score;
+      best = c;
+    }
+  }
+  return best;
+}
 
 std::unique_ptr<Plan> make_shard(const Plan& full, int rank, int world, const PlanOptions& opt, std::int64_t* lo,
                                  std::int64_t* hi, std::string* axis) {

@@ -81,6 +81,7 @@ struct GettBinding {
   std::int64_t a_mo = 0, a_mi = 0, a_kb = 0, b_no = 0, b_ni = 0, b_ka = 0;
   std::int64_t c_mo = 0, c_mi = 0, c_no = 0, c_ni = 0;
   std::string role_names;  // "mo=a mi=b ..." for describe()
+  std::string shard_m;     // canonical name of the M index shards split (outer M index)
   // operands whose unit-stride index is not their contracted one are repacked
   // per execute into a plan buffer laid out [mo][mi][kB][kA] (A) or
   // [no][ni][kA][kB] (B); *_src are the source strides in that dim order
@@ -208,6 +209,9 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
 // Shard plan for rank/world along the family's shard axis.
 std::unique_ptr<Plan> make_shard(const Plan& full, int rank, int world, const PlanOptions& opt,
                                  std::int64_t* lo, std::int64_t* hi, std::string* axis);
+
+// Chunks of the host pipeline (fe_plan_execute_host) for this plan.
+int pipe_chunks(const Plan& p, int dflt);
 
 std::string describe(const Plan& plan);  // JSON
 

@@ -34,6 +34,9 @@ def _worker(rank, world, port, results):
         "C4": dict(einsum=C.tensor_train(n=8192)),
         "C5": dict(kernel=C.wave_kernel(E=40_000)),
         "C1-f32": dict(einsum=C.fem_grad(E=20_004, dtype="float32")),  # fp32: shards in fours
+        "matmul": dict(einsum={"i_out": ["a", "c"], "i_in": [["a", "b"], ["b", "c"]],  # split-form GETT
+                               "args": [[{"name": "A", "shape": [1024, 256], "dtype": "float64"},
+                                         {"name": "B", "shape": [256, 96], "dtype": "float64"}]]}),
         "generic": dict(einsum={"i_out": ["i", "j"], "i_in": [["i", "k"], ["k", "j"]],
                                 "args": [[{"name": "A", "shape": [6, 3], "dtype": "float64"},
                                           {"name": "B", "shape": [3, 5], "dtype": "float64"}]]}),

@@ -505,7 +505,8 @@ std::unique_ptr<HostPipe> make_pipe(const fe_plan_s& h) {
   std::int64_t bytes = 0;
   for (const auto& L : p.leaves) bytes += L.bytes();
   for (const auto& O : p.outputs) bytes += O.bytes();
-  if (bytes < (std::int64_t{256} << 20)) return nullptr;
+  const char* thr = std::getenv("FE_PIPE_MIN_MB");
+  if (bytes < (static_cast<std::int64_t>(thr ? std::atoi(thr) : 64) << 20)) return nullptr;
   // 8 chunks (measured on the suite: 8 and 16 tie, 32 loses to per-chunk
   // launch and copy overheads); FE_PIPE_CHUNKS overrides for experiments
   const int chunks = std::getenv("FE_PIPE_CHUNKS") ? std::max(2, std::atoi(std::getenv("FE_PIPE_CHUNKS")))

@@ -111,7 +111,7 @@ int fe_plan_num_outputs(fe_plan_t plan);
 int fe_plan_execute(fe_plan_t plan, const void* const* d_in, void* const* d_out, void* stream);
 /* end-to-end: host inputs -> H2D -> kernels -> D2H into host outputs, ordered
  * on `stream` (device staging buffers are owned by the plan; not
- * synchronized). Plans above 256 MB run as a pipeline of 8 chunks along the
+ * synchronized). Plans above 64 MB run as a pipeline of chunks (8; GETT: by wave fill) along the
  * shard axis: chunk k's H2D, chunk k-1's kernels and chunk k-2's D2H overlap
  * on internal streams (host buffers should be pinned for the copies to
  * overlap); `stream` resumes after the last D2H. */

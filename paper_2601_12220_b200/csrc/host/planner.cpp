@@ -656,18 +656,22 @@ bool bind_gett_split(Plan& p, std::string* why) {
     *why = "repeated indices";
     return false;
   }
-  std::vector<std::string> K, M0, N1;  // K in operand 0's order
+  std::vector<std::string> K, M0, N1, Z;  // K in operand 0's order; Z: batch (in A, B and C)
   for (const auto& x : l0) {
     const bool in1 = s1.count(x) > 0, ino = so.count(x) > 0;
     if (in1 && ino) {
-      *why = "batch index";
-      return false;
+      Z.push_back(x);
+      continue;
     }
     if (!in1 && !ino) {
       *why = "index summed within one operand";
       return false;
     }
     (in1 ? K : M0).push_back(x);
+  }
+  if (Z.size() > 1) {
+    *why = "more than one batch index";
+    return false;
   }
   for (const auto& x : l1) {
     if (s0.count(x)) continue;
@@ -775,9 +779,24 @@ bool bind_gett_split(Plan& p, std::string* why) {
     return false;
   }
   if (!gett_rows(p, g, sa, sb, why)) return false;
+  VD zd;  // batch dim (extent 1 when there is none)
+  if (!Z.empty()) {
+    zd = vd_of(Z[0]);
+    for (const auto& r : g.rows)
+      if (r.a_alpha >= 0 || r.b_alpha >= 0) {
+        *why = "alpha*X+beta operands with a batch index";
+        return false;
+      }
+  }
+  g.nz = zd.ext;
+  g.c_z = zd.c;
   // A: kA unit stride, other strides even (16-byte TMA strides); B: kB
-  g.pack_a = g.a_f32 || ka.a != 1 || mo.a % 2 || mi.a % 2 || kb.a % 2;
-  g.pack_b = g.b_f32 || kb.b != 1 || no.b % 2 || ni.b % 2 || ka.b % 2;
+  g.pack_a = g.a_f32 || ka.a != 1 || mo.a % 2 || mi.a % 2 || kb.a % 2 || zd.a % 2;
+  g.pack_b = g.b_f32 || kb.b != 1 || no.b % 2 || ni.b % 2 || ka.b % 2 || zd.b % 2;
+  g.a_z_src = zd.a;
+  g.b_z_src = zd.b;
+  g.a_z = g.pack_a ? g.ext_mo * g.ext_mi * g.ext_kb * g.ext_ka : zd.a;
+  g.b_z = g.pack_b ? g.ext_no * g.ext_ni * g.ext_ka * g.ext_kb : zd.b;
   if (g.pack_a) {
     const std::int64_t src[4] = {mo.a, mi.a, kb.a, ka.a};
     std::copy(src, src + 4, g.a_src);
@@ -810,7 +829,7 @@ bool bind_gett_split(Plan& p, std::string* why) {
     return r;
   };
   g.shard_m = M[0];
-  g.role_names = "split M=" + names(M) + " (" + std::to_string(g.ext_mo) + "x" + std::to_string(g.ext_mi) + ") N=" +
+  g.role_names = std::string(Z.empty() ? "" : "batch " + Z[0] + " (" + std::to_string(g.nz) + ") ") + "split M=" + names(M) + " (" + std::to_string(g.ext_mo) + "x" + std::to_string(g.ext_mi) + ") N=" +
                  names(N) + " (" + std::to_string(g.ext_no) + "x" + std::to_string(g.ext_ni) + ") K=" + names(K) +
                  " (" + std::to_string(g.ext_kb) + "x" + std::to_string(g.ext_ka) + ")" + (g.pack_a ? " packA" : "") +
                  (g.pack_b ? " packB" : "") + (g.a_f32 || g.b_f32 || g.c_f32 ? " f32io" : "");
@@ -1459,15 +1478,15 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
     const GettBinding& g = p.gett;
     if (g.pack_a)
       cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_pack_a),
-                            sizeof(double) * static_cast<size_t>(g.ext_mo * g.ext_mi * g.ext_ka * g.ext_kb)),
+                            sizeof(double) * static_cast<size_t>(g.ext_mo * g.ext_mi * g.ext_ka * g.ext_kb * g.nz)),
                  "cudaMalloc(gett packed A)");
     if (g.pack_b)
       cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_pack_b),
-                            sizeof(double) * static_cast<size_t>(g.ext_no * g.ext_ni * g.ext_ka * g.ext_kb)),
+                            sizeof(double) * static_cast<size_t>(g.ext_no * g.ext_ni * g.ext_ka * g.ext_kb * g.nz)),
                  "cudaMalloc(gett packed B)");
     if (g.c_f32)
       cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_cbuf),
-                            sizeof(double) * static_cast<size_t>(g.ext_mo * g.ext_mi * g.ext_no * g.ext_ni)),
+                            sizeof(double) * static_cast<size_t>(g.ext_mo * g.ext_mi * g.ext_no * g.ext_ni * g.nz)),
                  "cudaMalloc(gett f64 result)");
   }
 }
@@ -1704,19 +1723,25 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         L.B = static_cast<const double*>(d_in[r.b_leaf]);
         if (b.pack_a) {
           const std::int64_t ext[4] = {b.ext_mo, b.ext_mi, b.ext_kb, b.ext_ka};
-          cuda_check(b.a_f32 ? permute4_widen(static_cast<const float*>(d_in[r.a_leaf]), plan.d_pack_a, ext, b.a_src, stream)
-                             : permute4(L.A, plan.d_pack_a, ext, b.a_src, stream),
+          cuda_check(b.a_f32 ? permute4_widen(static_cast<const float*>(d_in[r.a_leaf]), plan.d_pack_a, ext, b.a_src, stream,
+                                              b.nz, b.a_z_src)
+                             : permute4(L.A, plan.d_pack_a, ext, b.a_src, stream, b.nz, b.a_z_src),
                      "gett pack A");
           L.A = plan.d_pack_a;
         }
         if (b.pack_b) {
           const std::int64_t ext[4] = {b.ext_no, b.ext_ni, b.ext_ka, b.ext_kb};
-          cuda_check(b.b_f32 ? permute4_widen(static_cast<const float*>(d_in[r.b_leaf]), plan.d_pack_b, ext, b.b_src, stream)
-                             : permute4(L.B, plan.d_pack_b, ext, b.b_src, stream),
+          cuda_check(b.b_f32 ? permute4_widen(static_cast<const float*>(d_in[r.b_leaf]), plan.d_pack_b, ext, b.b_src, stream,
+                                              b.nz, b.b_z_src)
+                             : permute4(L.B, plan.d_pack_b, ext, b.b_src, stream, b.nz, b.b_z_src),
                      "gett pack B");
           L.B = plan.d_pack_b;
         }
         L.C = b.c_f32 ? plan.d_cbuf : static_cast<double*>(d_out[r.out_row]);
+        L.nz = b.nz;
+        L.a_z = b.a_z;
+        L.b_z = b.b_z;
+        L.c_z = b.c_z;
         L.a_alpha = r.a_alpha;
         L.a_beta = r.a_beta;
         L.b_alpha = r.b_alpha;
@@ -1729,7 +1754,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         cuda_check(launch_gett(L, stream), "gett kernel");
         if (b.c_f32)
           cuda_check(narrow_f64_f32(plan.d_cbuf, static_cast<float*>(d_out[r.out_row]),
-                                    b.ext_mo * b.ext_mi * b.ext_no * b.ext_ni, stream),
+                                    b.ext_mo * b.ext_mi * b.ext_no * b.ext_ni * b.nz, stream),
                      "gett narrow C");
       }
       return;

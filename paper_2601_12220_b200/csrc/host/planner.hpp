@@ -90,6 +90,10 @@ struct GettBinding {
   // float32 in double, so the f64 DMMA path is its arithmetic); an fp32
   // output is accumulated in d_cbuf and narrowed once
   bool a_f32 = false, b_f32 = false, c_f32 = false;
+  // batch index (in A, B and C; split form only): nz values; kernel strides
+  // a_z / b_z (after a repack: the packed block size), source strides for
+  // the repack, C stride
+  std::int64_t nz = 1, a_z = 0, b_z = 0, a_z_src = 0, b_z_src = 0, c_z = 0;
   std::int64_t a_src[4] = {0, 0, 0, 0}, b_src[4] = {0, 0, 0, 0};
   struct Row {
     int a_leaf, b_leaf, out_row;

@@ -64,6 +64,7 @@ struct GettDev {
   int vec_c;  // C rows allow 16-byte stores of (n, n+1) pairs
   double kdim;         // |K| = ext_ka * ext_kb
   int stages, group;  // group: side of the square raster block (tiles sharing A/B slices in L2)
+  std::int64_t nz, c_z;  // batch count (an index of A, B and C) and its C stride; 5-D maps when nz > 1
 };
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1,
@@ -72,6 +73,15 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, s
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
           ptx::smem_addr(dst)),
       "l"(map), "r"(ptx::smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1,
+                                            int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(
+          ptx::smem_addr(dst)),
+      "l"(map), "r"(ptx::smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
 
@@ -87,7 +97,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* empty = full + S;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const std::int64_t ntiles = p.mo * p.no;
+  const std::int64_t per_z = p.mo * p.no;  // tiles per batch value
+  const std::int64_t ntiles = per_z * p.nz;
   const std::int64_t ksteps = p.ka_steps * p.kb_steps;
 
   if (threadIdx.x == 0) {
@@ -122,7 +133,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     std::int64_t it = 0;
     for (std::int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       std::int64_t mo, no;
-      tile_coords(t, mo, no);
+      const int z = static_cast<int>(t / per_z);
+      tile_coords(t - z * per_z, mo, no);
       for (std::int64_t ks = 0; ks < ksteps; ++ks, ++it) {
         const int s = static_cast<int>(it % S);
         const std::uint32_t round = static_cast<std::uint32_t>(it / S);
@@ -134,8 +146,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // A dims (kA, mi, kB, mo) -> image [mo2][kB][mi][kA] (64-byte rows, 64B swizzle);
         // B dims (kB, ni, kA, no) -> image [no2][kA][ni][kB] (32-byte rows, 32B swizzle)
         // boxes of two mo (no) values; an odd last one reads zeros out of bounds
-        tma_load_4d(st, &tmA, &full[s], ka0, 0, kb0, static_cast<int>(mo * MT));
-        tma_load_4d(st + kTileBytes, &tmB, &full[s], kb0, 0, ka0, static_cast<int>(no * NT));
+        if (p.nz > 1) {
+          tma_load_5d(st, &tmA, &full[s], ka0, 0, kb0, static_cast<int>(mo * MT), z);
+          tma_load_5d(st + kTileBytes, &tmB, &full[s], kb0, 0, ka0, static_cast<int>(no * NT), z);
+        } else {
+          tma_load_4d(st, &tmA, &full[s], ka0, 0, kb0, static_cast<int>(mo * MT));
+          tma_load_4d(st + kTileBytes, &tmB, &full[s], kb0, 0, ka0, static_cast<int>(no * NT));
+        }
       }
     }
     return;
@@ -164,7 +181,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::int64_t it = 0;
   for (std::int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     std::int64_t mo, no;
-    tile_coords(t, mo, no);
+    const std::int64_t z = t / per_z;
+    tile_coords(t - z * per_z, mo, no);
     double acc[3][9][2];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -209,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // extent, filled with zeros by TMA) are not stored
     const std::int64_t gmo = mo * MT + mo_l, gno = no * NT + wn;
     if (gmo >= p.ext_mo || gno >= p.ext_no) continue;
-    double* cbase = p.C + gmo * p.c_mo + gno * p.c_no;
+    double* cbase = p.C + z * p.c_z + gmo * p.c_mo + gno * p.c_no;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       const int m = m0 + i * 8 + qrow;
@@ -273,18 +291,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-bool make_map(CUtensorMap* map, const double* base, const std::uint64_t dims[4], const std::uint64_t strides_el[4],
-              const std::uint32_t box[4], CUtensorMapSwizzle swizzle) {
+// rank 4, or 5 with a batch dim (box 1) appended
+bool make_map(CUtensorMap* map, const double* base, const std::uint64_t dims[5], const std::uint64_t strides_el[5],
+              const std::uint32_t box[5], CUtensorMapSwizzle swizzle, int rank = 4) {
   auto enc = encode_fn();
   if (!enc) return false;
-  cuuint64_t gdim[4], gstride[3];
-  cuuint32_t bdim[4], estr[4] = {1, 1, 1, 1};
-  for (int d = 0; d < 4; ++d) {
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t bdim[5], estr[5] = {1, 1, 1, 1, 1};
+  for (int d = 0; d < rank; ++d) {
     gdim[d] = dims[d];
     bdim[d] = box[d];
   }
-  for (int d = 1; d < 4; ++d) gstride[d - 1] = strides_el[d] * 8;
-  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), gdim, gstride, bdim, estr,
+  for (int d = 1; d < rank; ++d) gstride[d - 1] = strides_el[d] * 8;
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, static_cast<cuuint32_t>(rank), const_cast<double*>(base), gdim, gstride, bdim, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -305,21 +324,26 @@ bool gett_supported(std::int64_t ext_mi, std::int64_t ext_ni, std::int64_t ext_k
 int launch_gett(const GettLaunch& L, void* stream) {
   if (!gett_supported(L.ext_mi, L.ext_ni, L.ext_ka, L.ext_kb)) return cudaErrorInvalidValue;
   CUtensorMap tmA, tmB;
+  const std::int64_t nz = L.nz > 1 ? L.nz : 1;
+  const int rank = nz > 1 ? 5 : 4;
+  if (nz > 1 && (L.a_alpha >= 0 || L.b_alpha >= 0)) return cudaErrorInvalidValue;  // row sums are per batch
   {
-    const std::uint64_t dims[4] = {static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_mi),
-                                   static_cast<std::uint64_t>(L.ext_kb), static_cast<std::uint64_t>(L.ext_mo)};
-    const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.a_mi), static_cast<std::uint64_t>(L.a_kb),
-                                  static_cast<std::uint64_t>(L.a_mo)};
-    const std::uint32_t box[4] = {KA, EXT, KB, MT};
-    if (!make_map(&tmA, L.A, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+    const std::uint64_t dims[5] = {static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_mi),
+                                   static_cast<std::uint64_t>(L.ext_kb), static_cast<std::uint64_t>(L.ext_mo),
+                                   static_cast<std::uint64_t>(nz)};
+    const std::uint64_t str[5] = {1, static_cast<std::uint64_t>(L.a_mi), static_cast<std::uint64_t>(L.a_kb),
+                                  static_cast<std::uint64_t>(L.a_mo), static_cast<std::uint64_t>(L.a_z)};
+    const std::uint32_t box[5] = {KA, EXT, KB, MT, 1};
+    if (!make_map(&tmA, L.A, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B, rank)) return cudaErrorInvalidValue;
   }
   {
-    const std::uint64_t dims[4] = {static_cast<std::uint64_t>(L.ext_kb), static_cast<std::uint64_t>(L.ext_ni),
-                                   static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_no)};
-    const std::uint64_t str[4] = {1, static_cast<std::uint64_t>(L.b_ni), static_cast<std::uint64_t>(L.b_ka),
-                                  static_cast<std::uint64_t>(L.b_no)};
-    const std::uint32_t box[4] = {KB, EXT, KA, NT};
-    if (!make_map(&tmB, L.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_32B)) return cudaErrorInvalidValue;
+    const std::uint64_t dims[5] = {static_cast<std::uint64_t>(L.ext_kb), static_cast<std::uint64_t>(L.ext_ni),
+                                   static_cast<std::uint64_t>(L.ext_ka), static_cast<std::uint64_t>(L.ext_no),
+                                   static_cast<std::uint64_t>(nz)};
+    const std::uint64_t str[5] = {1, static_cast<std::uint64_t>(L.b_ni), static_cast<std::uint64_t>(L.b_ka),
+                                  static_cast<std::uint64_t>(L.b_no), static_cast<std::uint64_t>(L.b_z)};
+    const std::uint32_t box[5] = {KB, EXT, KA, NT, 1};
+    if (!make_map(&tmB, L.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_32B, rank)) return cudaErrorInvalidValue;
   }
   GettDev d{};
   d.mo = (L.ext_mo + MT - 1) / MT;
@@ -328,7 +352,7 @@ int launch_gett(const GettLaunch& L, void* stream) {
   d.ext_no = L.ext_no;
   d.ka_steps = (L.ext_ka + KA - 1) / KA;
   d.kb_steps = (L.ext_kb + KB - 1) / KB;
-  d.vec_c = L.c_ni == 1 && L.c_mi % 2 == 0 && L.c_mo % 2 == 0 && L.c_no % 2 == 0 &&
+  d.vec_c = L.c_ni == 1 && L.c_mi % 2 == 0 && L.c_mo % 2 == 0 && L.c_no % 2 == 0 && L.c_z % 2 == 0 &&
             (reinterpret_cast<std::uintptr_t>(L.C) & 15) == 0;
   d.c_mo = L.c_mo;
   d.c_mi = L.c_mi;
@@ -354,6 +378,8 @@ int launch_gett(const GettLaunch& L, void* stream) {
     rowsum_kernel<<<static_cast<int>((rb * 32 + 255) / 256), 256, 0, st>>>(
         L.B, L.scratch + ra, L.ext_no, L.ext_ni, L.b_no, L.b_ni, L.ext_ka, L.ext_kb, L.b_ka, 1);
   }
+  d.nz = nz;
+  d.c_z = L.c_z;
   d.stages = L.stages > 0 ? L.stages : 3;
   d.group = L.group > 0 ? L.group : 6;
   const size_t smem = 1024 + static_cast<size_t>(d.stages) * 2 * kTileBytes + 16 * d.stages;
@@ -366,7 +392,7 @@ int launch_gett(const GettLaunch& L, void* stream) {
   if (per_sm < 1) per_sm = 1;
   std::int64_t grid = static_cast<std::int64_t>(sms) * per_sm;
   if (L.grid > 0) grid = L.grid;
-  if (grid > d.mo * d.no) grid = d.mo * d.no;
+  if (grid > d.mo * d.no * nz) grid = d.mo * d.no * nz;
   gett_kernel<<<static_cast<int>(grid), kThreads, smem, static_cast<cudaStream_t>(stream)>>>(d, tmA, tmB);
   return cudaGetLastError();
 }

@@ -213,6 +213,9 @@ struct GettLaunch {
   const double* coef;
   double* scratch;  // ext_mo*ext_mi + ext_no*ext_ni doubles (affine operands' K-sums)
   int stages, group, grid;
+  // batch: an index of A, B and C (nz values, strides a_z / b_z / c_z; no
+  // affine operands); nz <= 1 = none
+  std::int64_t nz, a_z, b_z, c_z;
 };
 
 int launch_gett(const GettLaunch& p, void* stream);
@@ -265,9 +268,12 @@ int flush_l2(void* scratch, std::int64_t bytes, void* stream);
 // dst[i0][i1][i2][i3] (contiguous, extents ext[0..3]) = src[sum_d i_d * src_stride[d]]:
 // repacks a strided operand into a kernel's layout (GETT operands whose
 // unit-stride index is not a contracted one)
-int permute4(const double* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream);
+// nz > 1: a batch of nz blocks, src stride src_z, packed back to back in dst
+int permute4(const double* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream,
+             std::int64_t nz = 1, std::int64_t src_z = 0);
 // the same from an fp32 source, widened to fp64; and a dense fp64 -> fp32 copy
-int permute4_widen(const float* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream);
+int permute4_widen(const float* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream,
+                   std::int64_t nz = 1, std::int64_t src_z = 0);
 int narrow_f64_f32(const double* src, float* dst, std::int64_t n, void* stream);
 // which: 0 = DFMA (CUDA cores), 1 = DMMA m8n8k4 (FP64 tensor cores)
 int fp64_peak(int which, double* tflops);

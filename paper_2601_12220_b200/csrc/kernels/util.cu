@@ -143,6 +143,7 @@ struct Permute4 {
   double* dst;
   std::int64_t ext[4], ss[4], ds[4];
   int u;  // dst dim whose src stride is 1 (-1: none)
+  std::int64_t nz, sz;  // batch: nz copies, src stride sz, dst stride = the 4-D block size
 };
 
 template <typename T>
@@ -153,30 +154,35 @@ __global__ void permute4_tiled(const __grid_constant__ Permute4<T> p) {
   int oa = -1, ob = -1;
   for (int d = 0; d < 3; ++d)
     if (d != u) (oa < 0 ? oa : ob) = d;
-  const std::int64_t z = blockIdx.z;
-  const std::int64_t ia = z / p.ext[ob], ib = z - ia * p.ext[ob];
+  const std::int64_t planes = p.ext[oa] * p.ext[ob], block = p.ext[0] * p.ext[1] * p.ext[2] * p.ext[3];
   const std::int64_t x0 = static_cast<std::int64_t>(blockIdx.x) * 32, y0 = static_cast<std::int64_t>(blockIdx.y) * 32;
-  const std::int64_t base_s = ia * p.ss[oa] + ib * p.ss[ob];
-  const std::int64_t base_d = ia * p.ds[oa] + ib * p.ds[ob];
-  // read: consecutive threads walk the src unit-stride dim u
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const std::int64_t x = x0 + r, y = y0 + threadIdx.x;
-    if (x < p.ext[3] && y < p.ext[u]) tile[r][threadIdx.x] = static_cast<double>(__ldg(p.src + base_s + x * p.ss[3] + y));
-  }
-  __syncthreads();
-  // write: consecutive threads walk the dst inner dim 3
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const std::int64_t y = y0 + r, x = x0 + threadIdx.x;
-    if (x < p.ext[3] && y < p.ext[u]) p.dst[base_d + y * p.ds[u] + x] = tile[threadIdx.x][r];
+  for (std::int64_t z = blockIdx.z; z < planes * p.nz; z += gridDim.z) {
+    const std::int64_t bz = z / planes, zr = z - bz * planes;
+    const std::int64_t ia = zr / p.ext[ob], ib = zr - ia * p.ext[ob];
+    const std::int64_t base_s = bz * p.sz + ia * p.ss[oa] + ib * p.ss[ob];
+    const std::int64_t base_d = bz * block + ia * p.ds[oa] + ib * p.ds[ob];
+    // read: consecutive threads walk the src unit-stride dim u
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const std::int64_t x = x0 + r, y = y0 + threadIdx.x;
+      if (x < p.ext[3] && y < p.ext[u]) tile[r][threadIdx.x] = static_cast<double>(__ldg(p.src + base_s + x * p.ss[3] + y));
+    }
+    __syncthreads();
+    // write: consecutive threads walk the dst inner dim 3
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const std::int64_t y = y0 + r, x = x0 + threadIdx.x;
+      if (x < p.ext[3] && y < p.ext[u]) p.dst[base_d + y * p.ds[u] + x] = tile[threadIdx.x][r];
+    }
+    __syncthreads();
   }
 }
 
 template <typename T>
 __global__ void permute4_plain(const __grid_constant__ Permute4<T> p) {
   const std::int64_t n = p.ext[0] * p.ext[1] * p.ext[2] * p.ext[3];
-  for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < n;
+  for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < n * p.nz;
        t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-    std::int64_t r = t, off = 0;
+    const std::int64_t bz = t / n;
+    std::int64_t r = t - bz * n, off = bz * p.sz;
     for (int d = 3; d >= 0; --d) {
       const std::int64_t i = r % p.ext[d];
       r /= p.ext[d];
@@ -201,11 +207,14 @@ __global__ void convert_kernel(const S* __restrict__ src, D* __restrict__ dst, s
 }
 
 template <typename T>
-int permute4_t(const T* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream) {
+int permute4_t(const T* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream,
+               std::int64_t nz, std::int64_t src_z) {
   Permute4<T> p{};
   p.src = src;
   p.dst = dst;
   p.u = -1;
+  p.nz = nz > 1 ? nz : 1;
+  p.sz = src_z;
   std::int64_t acc = 1;
   for (int d = 3; d >= 0; --d) {
     p.ext[d] = ext[d];
@@ -220,28 +229,32 @@ int permute4_t(const T* src, double* dst, const std::int64_t ext[4], const std::
     int oa = -1, ob = -1;
     for (int d = 0; d < 3; ++d)
       if (d != p.u) (oa < 0 ? oa : ob) = d;
+    const std::int64_t gz = ext[oa] * ext[ob] * p.nz;
     const dim3 grid(static_cast<unsigned>((ext[3] + 31) / 32), static_cast<unsigned>((ext[p.u] + 31) / 32),
-                    static_cast<unsigned>(ext[oa] * ext[ob]));
+                    static_cast<unsigned>(gz < 65535 ? gz : 65535));
     permute4_tiled<T><<<grid, dim3(32, 8), 0, st>>>(p);
   } else {
     int sms = 148;
     device_sm_count(&sms);
     bool dense = true;
     for (int d = 0; d < 4; ++d) dense = dense && (ext[d] == 1 || p.ss[d] == p.ds[d]);
+    dense = dense && (p.nz == 1 || p.sz == acc);
     if (dense)
-      convert_kernel<T, double><<<sms * 8, 256, 0, st>>>(src, dst, acc);
+      convert_kernel<T, double><<<sms * 8, 256, 0, st>>>(src, dst, acc * p.nz);
     else
       permute4_plain<T><<<sms * 8, 256, 0, st>>>(p);
   }
   return cudaGetLastError();
 }
 
-int permute4(const double* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream) {
-  return permute4_t<double>(src, dst, ext, src_stride, stream);
+int permute4(const double* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream,
+             std::int64_t nz, std::int64_t src_z) {
+  return permute4_t<double>(src, dst, ext, src_stride, stream, nz, src_z);
 }
 
-int permute4_widen(const float* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream) {
-  return permute4_t<float>(src, dst, ext, src_stride, stream);
+int permute4_widen(const float* src, double* dst, const std::int64_t ext[4], const std::int64_t src_stride[4], void* stream,
+                   std::int64_t nz, std::int64_t src_z) {
+  return permute4_t<float>(src, dst, ext, src_stride, stream, nz, src_z);
 }
 
 int narrow_f64_f32(const double* src, float* dst, std::int64_t n, void* stream) {

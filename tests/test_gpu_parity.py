@@ -328,6 +328,31 @@ def test_gett_split_groups_matmul_shapes(fe, ref, torch_cuda):
             assert np.array_equal(got, want), k
 
 
+def test_gett_batched(fe, ref, torch_cuda):
+    """A batch index (in A, B and C: batched matmul) rides on a fifth TMA
+    dimension and the tile scheduler; repacks run per batch value in one
+    launch. Exact on dyadic data."""
+    m = lambda n, s, dt="float64": {"name": n, "shape": s, "dtype": dt}  # noqa: E731
+    cases = [
+        {"i_out": ["z", "a", "c"], "i_in": [["z", "a", "b"], ["z", "b", "c"]], "args": [[m("A", [4, 64, 96]), m("B", [4, 96, 48])]]},
+        {"i_out": ["a", "z", "c"], "i_in": [["a", "z", "b"], ["b", "z", "c"]], "args": [[m("A", [72, 3, 64]), m("B", [64, 3, 48])]]},
+        {"i_out": ["z", "a", "b", "c"], "i_in": [["z", "a", "b", "k"], ["z", "k", "c"]],
+         "args": [[m("A", [3, 30, 40, 64]), m("B", [3, 64, 48])]]},
+        {"i_out": ["z", "a", "c"], "i_in": [["z", "a", "b"], ["z", "b", "c"]],
+         "args": [[m("A", [5, 50, 64], "float32"), m("B", [5, 64, 72], "float32")]]},
+    ]
+    for k, e in enumerate(cases):
+        plan = fe.Plan(einsum=e)
+        assert plan.info["transform"] == "gett_dmma/v1", (k, plan.info)
+        b = ref.random_bindings(e, 60 + k)
+        got = run_plan(torch_cuda, plan, b)[0]
+        want = ref.evaluate(e, b)[0].real
+        if got.dtype == np.float32:
+            assert np.array_equal(got, want.astype(np.float32)), k
+        else:
+            assert np.array_equal(got, want), k
+
+
 def test_gett_fp32_operands_widened(fe, ref, torch_cuda):
     """float32 TCCG operands run on the f64 DMMA GETT (widened in the pack pass,
     as the reference computes float32 in double); an fp32 output is narrowed

@@ -53,6 +53,7 @@ const char* family_transform(Family f) {
     case Family::gett: return "gett_dmma/v1";
     case Family::tt: return "tt/v1";
     case Family::hex: return "hex_sumfact/v1";
+    case Family::path: return "path/v1";
   }
   return "generic/v1";
 }
@@ -1303,6 +1304,152 @@ void upload_tables(Plan& p, GenericLaunch& g, const BatchedEinsum& e, bool dry_r
   g.coef = p.d_coef;
 }
 
+// Contraction path for einsums of three or more operands with no tuned family
+// of their own: the cheapest pairwise order (the DP of optimal_path_flops,
+// the opt_einsum convention the roofline counts in) executed as a chain of
+// 2-operand plans, each on its own tuned family when one binds (GETT: M / N /
+// K / batch groups of one or two indices) and on the generic kernel
+// otherwise; taken when the path costs under a quarter of the naive sum.
+// Intermediates are fp64 plan buffers. The summation order differs from the reference's naive
+// sum (like every tuned family: the 1e-12 bar); exact on dyadic data while
+// partial sums stay below 2^53.
+bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
+  const BatchedEinsum& e = p.skel;
+  const int n = e.n();
+  if (e.b() != 1 || n < 3 || n > 12 || p.complex_mode || p.functional || !p.tabs.empty()) {
+    *why = "path: one row of 3..12 plain real operands";
+    return false;
+  }
+  for (int k = 0; k < n; ++k)
+    if (p.ops[static_cast<size_t>(k)].kind != OPK_PLAIN || leaf_info(p, p.ops[static_cast<size_t>(k)].leaf).storage != ST_F64) {
+      *why = "path: f64 plain operands only";
+      return false;
+    }
+  if (p.outputs[0].storage != ST_F64) {
+    *why = "path: f64 output only";
+    return false;
+  }
+  // every index in at least two places (operands, output); none repeated in an operand
+  std::map<std::string, int> uses;
+  for (int k = 0; k < n; ++k) {
+    std::set<std::string> seen;
+    for (const auto& x : e.i_in[k]) {
+      if (!seen.insert(x).second) {
+        *why = "path: repeated index in an operand";
+        return false;
+      }
+      ++uses[x];
+    }
+  }
+  for (const auto& x : e.i_out) ++uses[x];
+  for (const auto& [x, c] : uses)
+    if (c < 2) {
+      *why = "path: index summed within one operand";
+      return false;
+    }
+  const auto len = feinsum::index_lengths(e);
+  std::vector<std::set<std::string>> idx(static_cast<size_t>(n));
+  for (int k = 0; k < n; ++k) idx[static_cast<size_t>(k)].insert(e.i_in[k].begin(), e.i_in[k].end());
+  const std::set<std::string> out(e.i_out.begin(), e.i_out.end());
+  auto size_of = [&](const std::set<std::string>& st) {
+    double v = 1;
+    for (const auto& x : st) v *= static_cast<double>(len.at(x));
+    return v;
+  };
+  const int full = (1 << n) - 1;
+  std::vector<std::set<std::string>> keep(static_cast<size_t>(full) + 1);
+  for (int st = 1; st <= full; ++st) {
+    std::set<std::string> inside, outside = out;
+    for (int k = 0; k < n; ++k) (st >> k & 1 ? inside : outside).insert(idx[k].begin(), idx[k].end());
+    for (const auto& x : inside)
+      if (outside.count(x)) keep[static_cast<size_t>(st)].insert(x);
+  }
+  std::vector<double> cost(static_cast<size_t>(full) + 1, 0.0);
+  std::vector<int> split(static_cast<size_t>(full) + 1, 0);
+  for (int st = 1; st <= full; ++st) {
+    if ((st & (st - 1)) == 0) continue;
+    double best = INFINITY;
+    for (int a = (st - 1) & st; a > 0; a = (a - 1) & st) {
+      const int b = st ^ a;
+      if (a < b) continue;
+      std::set<std::string> all = keep[static_cast<size_t>(a)];
+      all.insert(keep[static_cast<size_t>(b)].begin(), keep[static_cast<size_t>(b)].end());
+      const double c = cost[static_cast<size_t>(a)] + cost[static_cast<size_t>(b)] +
+                       size_of(all) * (all.size() > keep[static_cast<size_t>(st)].size() ? 2.0 : 1.0);
+      if (c < best) {
+        best = c;
+        split[static_cast<size_t>(st)] = a;
+      }
+    }
+    cost[static_cast<size_t>(st)] = best;
+  }
+  if (cost[static_cast<size_t>(full)] * 4.0 >= feinsum::flop_count(e)) {
+    *why = "path: no cheaper than the naive sum";
+    return false;
+  }
+  // post-order build: an operand is (index list, meta, source)
+  struct Opnd {
+    feinsum::IndexList ix;
+    ArrayMeta meta;
+    int src;  // caller leaf, or -(1 + intermediate id)
+  };
+  std::vector<PathStep> steps;
+  std::vector<std::int64_t> offs;
+  std::int64_t bytes = 0;
+  PlanOptions so = opt;
+  so.force_transform.clear();
+  so.meta_override.clear();
+  std::function<Opnd(int)> build = [&](int st) -> Opnd {
+    if ((st & (st - 1)) == 0) {
+      int k = 0;
+      while (!(st >> k & 1)) ++k;
+      return Opnd{e.i_in[static_cast<size_t>(k)], e.args[0][static_cast<size_t>(k)], p.ops[static_cast<size_t>(k)].leaf};
+    }
+    const int a = split[static_cast<size_t>(st)], b = st ^ a;
+    const Opnd A = build(a), B = build(b);
+    Opnd R;
+    if (st == full) {
+      R.ix = e.i_out;
+    } else {
+      for (const auto* l : {&A.ix, &B.ix})
+        for (const auto& x : *l)
+          if (keep[static_cast<size_t>(st)].count(x) && std::find(R.ix.begin(), R.ix.end(), x) == R.ix.end()) R.ix.push_back(x);
+    }
+    const int id = static_cast<int>(offs.size());
+    R.meta.name = "_path_t" + std::to_string(id);
+    R.meta.dtype = Dtype::float64;
+    for (const auto& x : R.ix) R.meta.shape.push_back(len.at(x));
+    BatchedEinsum step;
+    step.i_out = R.ix;
+    step.i_in = {A.ix, B.ix};
+    step.args = {{A.meta, B.meta}};
+    PathStep ps;
+    ps.plan = make_plan(step, so);
+    for (const auto& L : ps.plan->leaves) ps.src.push_back(L.meta.name == A.meta.name ? A.src : B.src);
+    if (st == full) {
+      ps.out = -1;
+      R.src = 0;
+    } else {
+      ps.out = id;
+      offs.push_back(bytes);
+      bytes += (R.meta.num_elements() * 8 + 255) / 256 * 256;
+      R.src = -(1 + id);
+    }
+    steps.push_back(std::move(ps));
+    return R;
+  };
+  try {
+    build(full);
+  } catch (const std::exception& ex) {
+    *why = std::string("path: ") + ex.what();
+    return false;
+  }
+  p.path = std::move(steps);
+  p.inter_off = std::move(offs);
+  p.inter_bytes = bytes;
+  return true;
+}
+
 void finish_plan(Plan& p, const PlanOptions& opt) {
   const BatchedEinsum& e = p.skel;
   if (e.b() > kMaxRows) throw error(errc::usage, "more than 96 rows; spell the batch as an index");
@@ -1371,9 +1518,9 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
   }
 
   // kernel choice: forced > fact > first matching family > generic
-  std::vector<Family> order = {Family::fem_grad, Family::gett, Family::tt, Family::hex};
+  std::vector<Family> order = {Family::fem_grad, Family::gett, Family::tt, Family::hex, Family::path};
   auto family_of = [](const std::string& t) -> std::optional<Family> {
-    for (Family f : {Family::generic, Family::fem_grad, Family::gett, Family::tt, Family::hex})
+    for (Family f : {Family::generic, Family::fem_grad, Family::gett, Family::tt, Family::hex, Family::path})
       if (t == family_transform(f)) return f;
     return std::nullopt;
   };
@@ -1386,6 +1533,7 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
       case Family::gett: return bind_gett(p, &why);
       case Family::tt: return bind_tt(p, &why);
       case Family::hex: return bind_hex(p, &why);
+      case Family::path: return bind_path(p, opt, &why);
       default: return false;
     }
   };
@@ -1450,6 +1598,8 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
   for (int r = 0; r < e.b(); ++r) g.out_storage[r] = p.outputs[r].storage;
 
   upload_tables(p, g, e, opt.dry_run);
+  if (!opt.dry_run && p.family == Family::path && p.inter_bytes > 0)
+    cuda_check(cudaMalloc(&p.d_inter, static_cast<size_t>(p.inter_bytes)), "cudaMalloc(path intermediates)");
   for (size_t k = 0; k < p.tabs.size(); ++k) {
     Plan::TabOperand& t = p.tabs[k];
     const std::string src = tab_kernel_source(p, p.ops[static_cast<size_t>(t.op)], p.tab_leaves[k].meta, &t.leaf_slots);
@@ -1508,6 +1658,7 @@ Plan::~Plan() {
   if (d_pack_b) cudaFree(d_pack_b);
   if (d_cbuf) cudaFree(d_cbuf);
   if (d_tab) cudaFree(d_tab);
+  if (d_inter) cudaFree(d_inter);
 }
 
 std::unique_ptr<Plan> make_plan(const BatchedEinsum& e, const PlanOptions& opt) {
@@ -1637,6 +1788,16 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
     cuda_check(launch_tabulate(t, stream), "tabulate kernel");
   }
 
+  if (plan.family == Family::path) {
+    auto inter = [&](int id) { return static_cast<unsigned char*>(plan.d_inter) + plan.inter_off[static_cast<size_t>(id)]; };
+    for (const PathStep& st : plan.path) {
+      std::vector<const void*> in;
+      for (int src : st.src) in.push_back(src >= 0 ? d_in[src] : inter(-src - 1));
+      void* out = st.out < 0 ? d_out[0] : inter(st.out);
+      execute(*st.plan, in.data(), &out, stream);
+    }
+    return;
+  }
   if (plan.family == Family::fem_grad) {
     const FemBinding& f = plan.fem;
     FemGradLaunch L{};
@@ -1868,6 +2029,7 @@ std::string describe(const Plan& p) {
     case Family::gett: pipe = "dmma"; break;
     case Family::tt: pipe = (p.tt.fp32 && meta_int(p.meta, "tc", 1)) ? "tcgen05_tf32x3" : "dmma"; break;
     case Family::hex: pipe = "dfma"; break;
+    case Family::path: pipe = "dmma"; break;
     case Family::generic: pipe = "fma"; break;
   }
   v.set("pipe", Value::str(pipe));
@@ -1886,6 +2048,13 @@ std::string describe(const Plan& p) {
       }
       break;
     case Family::generic: launches += 1; break;
+    case Family::path:
+      for (const auto& st : p.path) {
+        const std::string d = describe(*st.plan);
+        const auto at = d.find("\"launches\":");
+        if (at != std::string::npos) launches += std::atoi(d.c_str() + at + 11);
+      }
+      break;
   }
   launches += static_cast<int>(p.tabs.size());
   v.set("launches", Value::num(launches));
@@ -1961,7 +2130,8 @@ std::string shard_index_of(const Plan& p) {
     case Family::gett:
       // the outer M index (4-index form: mo; split form: the M group's first)
       return p.canon.sigma_idx.at(p.gett.shard_m);
-    case Family::generic: break;
+    case Family::generic:
+    case Family::path: break;
   }
   return p.skel.i_out.empty() ? std::string() : p.skel.i_out[0];
 }

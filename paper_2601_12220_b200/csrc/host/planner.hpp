@@ -33,7 +33,7 @@ using feinsum::CanonResult;
 using feinsum::Dtype;
 using feinsum::OperandExpr;
 
-enum class Family { generic, fem_grad, gett, tt, hex };
+enum class Family { generic, fem_grad, gett, tt, hex, path };
 const char* family_transform(Family f);  // "generic/v1", "fem_grad/v1", ...
 
 struct PlanOptions {
@@ -122,6 +122,16 @@ struct HexBinding {
   std::vector<int> u, out_row;  // per canonical row
 };
 
+struct Plan;
+
+// One pairwise step of a contraction path (Family::path): a 2-operand plan
+// whose inputs are caller arrays or earlier intermediates.
+struct PathStep {
+  std::unique_ptr<Plan> plan;
+  std::vector<int> src;  // per step-plan input: caller leaf (>= 0) or intermediate -(1 + id)
+  int out = -1;          // intermediate id, or -1: the caller's output
+};
+
 struct Plan {
   // ---- what is computed ----
   BatchedEinsum skel;  // the caller's einsum (skeleton if functional)
@@ -165,6 +175,11 @@ struct Plan {
   GettBinding gett;
   TTBinding tt;
   HexBinding hex;
+  // contraction path (n >= 3 operands, every step on a tuned family)
+  std::vector<PathStep> path;
+  std::vector<std::int64_t> inter_off;  // intermediate id -> byte offset in d_inter
+  std::int64_t inter_bytes = 0;
+  void* d_inter = nullptr;
 
   // ---- costs ----
   double alg_flops = 0, operand_flops = 0, bytes = 0, ref_flops = 0;

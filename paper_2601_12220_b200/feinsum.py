@@ -315,12 +315,13 @@ def _run_wide(plan, bindings, device="cuda"):
     return [o.cpu().numpy().astype(np.complex128) for o in outs]
 
 
-def evaluate(e, bindings):
+def evaluate(e, bindings, options=None):
     """core.hpp evaluate: one complex128 array per row, computed on the GPU.
 
     ``bindings`` maps every array name of ``universe(e)`` to array data; values
     are uploaded unrounded (f64, or c128 if complex), like the reference's
-    complex<double> DenseArrays.
+    complex<double> DenseArrays. ``options``: extra plan options (e.g.
+    ``{"transform": "generic/v1"}`` for the bit-exact generic kernel).
     """
     errs = validate(e)
     if errs:
@@ -334,7 +335,7 @@ def evaluate(e, bindings):
             raise FeinsumError(1, "binding for array " + m["name"] + " has wrong element count")
         names.append(m["name"])
     _check(lib().fe_device_check())
-    opts = {"storage": "wide",
+    opts = {**(options or {}), "storage": "wide",
             "leaf_storage": {n: ("c128" if np.iscomplexobj(np.asarray(bindings[n])) else "f64") for n in names}}
     return _run_wide(Plan(einsum=e, options=opts), bindings)
 

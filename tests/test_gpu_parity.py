@@ -52,13 +52,52 @@ def test_device_visible(fe, torch_cuda):
     {"dtype_pool": ["float32", "float64", "int8", "int32"]},
 ])
 def test_generic_bit_exact_random(fe, ref, torch_cuda, params):
+    """The generic kernel reproduces feinsum::evaluate bit for bit."""
+    gen = {"transform": "generic/v1"}
     for seed in range(40):
         e = ref.generate_random(seed, **params)
         b = ref.random_bindings(e, seed + 17)
         want = ref.evaluate(e, b)
-        got = fe.evaluate(e, b)
+        got = fe.evaluate(e, b, gen)
         for g, w in zip(got, want):
             assert np.array_equal(g.reshape(-1), w.reshape(-1)), (seed, e)
+
+
+def test_default_plans_random(fe, ref, torch_cuda):
+    """Whatever the planner picks for random einsums (generic, a tuned family,
+    or a contraction path for three or more operands) stays within the fp64
+    bar of the reference."""
+    picked = set()
+    for seed in range(60):
+        e = ref.generate_random(seed, b_max=1, n_max=4, max_indices=6, shape_pool=[2, 3, 5, 8])
+        b = ref.random_bindings(e, seed + 23)
+        want = ref.evaluate(e, b)
+        got = fe.evaluate(e, b)
+        picked.add(fe.Plan(einsum=e, options={"dry_run": True}).info["transform"])
+        for g, w in zip(got, want):
+            assert rel_err(g, w) <= FP64_TOL, (seed, e)
+    assert "generic/v1" in picked
+
+
+def test_contraction_path(fe, ref, torch_cuda):
+    """Three- and four-operand chains run as pairwise GETT / generic steps in
+    the optimal order; within the fp64 bar of the naive reference sum."""
+    m = lambda n, s: {"name": n, "shape": s, "dtype": "float64"}  # noqa: E731
+    cases = [
+        {"i_out": ["a", "d"], "i_in": [["a", "b"], ["b", "c"], ["c", "d"]],
+         "args": [[m("A", [48, 64]), m("B", [64, 72]), m("C", [72, 40])]]},
+        {"i_out": ["a", "e"], "i_in": [["a", "b"], ["b", "c"], ["c", "d"], ["d", "e"]],
+         "args": [[m("A", [30, 64]), m("B", [64, 24]), m("C", [24, 48]), m("D", [48, 36])]]},
+        {"i_out": ["z", "a", "c"], "i_in": [["z", "a", "b"], ["b", "k"], ["z", "k", "c"]],
+         "args": [[m("A", [3, 40, 64]), m("B", [64, 64]), m("C", [3, 64, 30])]]},
+    ]
+    for k, e in enumerate(cases):
+        plan = fe.Plan(einsum=e)
+        assert plan.info["transform"] == "path/v1", (k, plan.info)
+        b = ref.random_bindings(e, 80 + k)
+        got = run_plan(torch_cuda, plan, b)[0]
+        want = ref.evaluate(e, b)[0].real
+        assert rel_err(got, want) <= FP64_TOL, k
 
 
 def test_generic_complex_bit_exact(fe, ref, torch_cuda):

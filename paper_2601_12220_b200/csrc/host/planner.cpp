@@ -1310,7 +1310,7 @@ void upload_tables(Plan& p, GenericLaunch& g, const BatchedEinsum& e, bool dry_r
 // 2-operand plans, each on its own tuned family when one binds (GETT: M / N /
 // K / batch groups of one or two indices) and on the generic kernel
 // otherwise; taken when the path costs under a quarter of the naive sum.
-// Intermediates are fp64 plan buffers. The summation order differs from the reference's naive
+// Intermediates are plan buffers in the operands' element type (f64 / f32). The summation order differs from the reference's naive
 // sum (like every tuned family: the 1e-12 bar); exact on dyadic data while
 // partial sums stay below 2^53.
 bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
@@ -1320,15 +1320,15 @@ bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
     *why = "path: one row of 3..12 plain real operands";
     return false;
   }
+  // one element type: f64, or f32 (fp32 intermediates, like any fp32 chain)
+  const int est = p.outputs[0].storage;
   for (int k = 0; k < n; ++k)
-    if (p.ops[static_cast<size_t>(k)].kind != OPK_PLAIN || leaf_info(p, p.ops[static_cast<size_t>(k)].leaf).storage != ST_F64) {
-      *why = "path: f64 plain operands only";
+    if (p.ops[static_cast<size_t>(k)].kind != OPK_PLAIN || leaf_info(p, p.ops[static_cast<size_t>(k)].leaf).storage != est ||
+        (est != ST_F64 && est != ST_F32)) {
+      *why = "path: plain operands, all f64 or all f32";
       return false;
     }
-  if (p.outputs[0].storage != ST_F64) {
-    *why = "path: f64 output only";
-    return false;
-  }
+  const std::int64_t esize = est == ST_F32 ? 4 : 8;
   // every index in at least two places (operands, output); none repeated in an operand
   std::map<std::string, int> uses;
   for (int k = 0; k < n; ++k) {
@@ -1417,7 +1417,7 @@ bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
     }
     const int id = static_cast<int>(offs.size());
     R.meta.name = "_path_t" + std::to_string(id);
-    R.meta.dtype = Dtype::float64;
+    R.meta.dtype = est == ST_F32 ? Dtype::float32 : Dtype::float64;
     for (const auto& x : R.ix) R.meta.shape.push_back(len.at(x));
     BatchedEinsum step;
     step.i_out = R.ix;
@@ -1432,7 +1432,7 @@ bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
     } else {
       ps.out = id;
       offs.push_back(bytes);
-      bytes += (R.meta.num_elements() * 8 + 255) / 256 * 256;
+      bytes += (R.meta.num_elements() * esize + 255) / 256 * 256;
       R.src = -(1 + id);
     }
     steps.push_back(std::move(ps));

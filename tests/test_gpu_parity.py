@@ -98,6 +98,12 @@ def test_contraction_path(fe, ref, torch_cuda):
         got = run_plan(torch_cuda, plan, b)[0]
         want = ref.evaluate(e, b)[0].real
         assert rel_err(got, want) <= FP64_TOL, k
+        # float32 arrays: fp32 intermediates, the fp32 bar
+        e32 = {**e, "args": [[{**a, "dtype": "float32"} for a in e["args"][0]]]}
+        plan = fe.Plan(einsum=e32)
+        assert plan.info["transform"] == "path/v1", (k, plan.info)
+        got = run_plan(torch_cuda, plan, b)[0]
+        assert got.dtype == np.float32 and rel_err(got, want) <= 1e-5, k
 
 
 def test_generic_complex_bit_exact(fe, ref, torch_cuda):

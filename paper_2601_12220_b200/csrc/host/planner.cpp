@@ -651,12 +651,49 @@ bool bind_gett_split(Plan& p, std::string* why) {
     *why = "not a 2-operand contraction";
     return false;
   }
-  const feinsum::IndexList &l0 = c.i_in[0], &l1 = c.i_in[1];
-  const std::set<std::string> s0(l0.begin(), l0.end()), s1(l1.begin(), l1.end()), so(c.i_out.begin(), c.i_out.end());
-  if (s0.size() != l0.size() || s1.size() != l1.size() || so.size() != c.i_out.size()) {
-    *why = "repeated indices";
-    return false;
+  {
+    const std::set<std::string> s0(c.i_in[0].begin(), c.i_in[0].end()), s1(c.i_in[1].begin(), c.i_in[1].end()),
+        so(c.i_out.begin(), c.i_out.end());
+    if (s0.size() != c.i_in[0].size() || s1.size() != c.i_in[1].size() || so.size() != c.i_out.size()) {
+      *why = "repeated indices";
+      return false;
+    }
   }
+  // fold indices that stay adjacent (same order) in every array holding them
+  // into one (TCCG's 6-index contractions: `dega,gfbc->abcdef` folds de and
+  // bc): the row-major offset of the pair is that of one index of the
+  // product extent, so no data moves
+  std::vector<std::string> L0 = c.i_in[0], L1 = c.i_in[1], LC = c.i_out;
+  std::map<std::string, std::int64_t> ex;
+  for (const auto& [x, v] : feinsum::index_lengths(c)) ex[x] = v;
+  for (bool merged = true; merged;) {
+    merged = false;
+    std::vector<std::vector<std::string>*> lists = {&L0, &L1, &LC};
+    for (auto* L : lists) {
+      for (size_t d = 0; d + 1 < L->size() && !merged; ++d) {
+        const std::string x = (*L)[d], y = (*L)[d + 1];
+        bool ok = true;
+        for (auto* M : lists) {
+          const auto px = std::find(M->begin(), M->end(), x), py = std::find(M->begin(), M->end(), y);
+          if ((px == M->end()) != (py == M->end())) ok = false;  // different groups
+          else if (px != M->end() && py != px + 1) ok = false;   // not adjacent in this array
+        }
+        if (!ok) continue;
+        const std::string xy = x + "+" + y;
+        ex[xy] = ex.at(x) * ex.at(y);
+        for (auto* M : lists) {
+          const auto px = std::find(M->begin(), M->end(), x);
+          if (px == M->end()) continue;
+          *px = xy;
+          M->erase(px + 1);
+        }
+        merged = true;
+      }
+      if (merged) break;
+    }
+  }
+  const feinsum::IndexList &l0 = L0, &l1 = L1;
+  const std::set<std::string> s0(l0.begin(), l0.end()), s1(l1.begin(), l1.end()), so(LC.begin(), LC.end());
   std::vector<std::string> K, M0, N1, Z;  // K in operand 0's order; Z: batch (in A, B and C)
   for (const auto& x : l0) {
     const bool in1 = s1.count(x) > 0, ino = so.count(x) > 0;
@@ -683,22 +720,23 @@ bool bind_gett_split(Plan& p, std::string* why) {
     N1.push_back(x);
   }
   if (K.empty() || M0.empty() || N1.empty() || K.size() > 2 || M0.size() > 2 || N1.size() > 2) {
-    *why = "index groups of one or two indices only";
+    *why = "index groups of one or two (folded) indices only";
     return false;
   }
-  const auto lens = feinsum::index_lengths(c);
-  auto strides = [&](const feinsum::IndexList& l, const std::vector<std::int64_t>& shape) {
+  const auto& lens = ex;
+  auto strides = [&](const std::vector<std::string>& l) {
     std::map<std::string, std::int64_t> m;
-    const auto st = row_major_strides(shape);
-    for (size_t d = 0; d < l.size(); ++d) m[l[d]] = st[d];
+    std::int64_t st = 1;
+    for (size_t d = l.size(); d-- > 0;) {
+      m[l[d]] = st;
+      st *= ex.at(l[d]);
+    }
     return m;
   };
-  std::vector<std::int64_t> shc;
-  for (const auto& x : c.i_out) shc.push_back(lens.at(x));
-  const auto st0 = strides(l0, c.args[0][0].shape), st1 = strides(l1, c.args[0][1].shape), stc = strides(c.i_out, shc);
+  const auto st0 = strides(L0), st1 = strides(L1), stc = strides(LC);
   // operand roles: B is the operand holding C's unit-stride index (coalesced
   // C stores run along the kernel's ni)
-  const bool swap = std::find(M0.begin(), M0.end(), c.i_out.back()) != M0.end();
+  const bool swap = std::find(M0.begin(), M0.end(), LC.back()) != M0.end();
   const int sa = swap ? 1 : 0, sb = 1 - sa;
   const auto& stA = swap ? st1 : st0;
   const auto& stB = swap ? st0 : st1;
@@ -829,7 +867,7 @@ bool bind_gett_split(Plan& p, std::string* why) {
     for (const auto& x : v) r += x;
     return r;
   };
-  g.shard_m = M[0];
+  g.shard_m = M[0].substr(0, M[0].find('+'));  // a folded pair shards along its outer index
   g.role_names = std::string(Z.empty() ? "" : "batch " + Z[0] + " (" + std::to_string(g.nz) + ") ") + "split M=" + names(M) + " (" + std::to_string(g.ext_mo) + "x" + std::to_string(g.ext_mi) + ") N=" +
                  names(N) + " (" + std::to_string(g.ext_no) + "x" + std::to_string(g.ext_ni) + ") K=" + names(K) +
                  " (" + std::to_string(g.ext_kb) + "x" + std::to_string(g.ext_ka) + ")" + (g.pack_a ? " packA" : "") +

@@ -373,6 +373,26 @@ def test_gett_split_groups_matmul_shapes(fe, ref, torch_cuda):
             assert np.array_equal(got, want), k
 
 
+def test_gett_folded_groups_tccg6(fe, ref, torch_cuda):
+    """6-index TCCG contractions whose groups have three indices fold the
+    ones that stay adjacent in every array (abcdef-dega-gfbc: de and bc)
+    into one dim; exact on dyadic data."""
+    m = lambda n, s: {"name": n, "shape": s, "dtype": "float64"}  # noqa: E731
+
+    def tc(out, a, b, L):
+        return {"i_out": list(out), "i_in": [list(a), list(b)], "args": [[m("A", [L[x] for x in a]), m("B", [L[x] for x in b])]]}
+    cases = [
+        tc("abcdef", "dega", "gfbc", {"a": 24, "b": 2, "c": 3, "d": 2, "e": 3, "f": 24, "g": 64}),
+        tc("abcdef", "gdab", "efgc", {"a": 4, "b": 6, "c": 3, "d": 2, "e": 2, "f": 12, "g": 64}),
+    ]
+    for k, e in enumerate(cases):
+        plan = fe.Plan(einsum=e)
+        assert plan.info["transform"] == "gett_dmma/v1", (k, plan.info)
+        b = ref.random_bindings(e, 90 + k)
+        got = run_plan(torch_cuda, plan, b)[0]
+        assert np.array_equal(got, ref.evaluate(e, b)[0].real), k
+
+
 def test_gett_batched(fe, ref, torch_cuda):
     """A batch index (in A, B and C: batched matmul) rides on a fifth TMA
     dimension and the tile scheduler; repacks run per batch value in one

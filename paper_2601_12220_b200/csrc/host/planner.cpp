@@ -1354,8 +1354,8 @@ void upload_tables(Plan& p, GenericLaunch& g, const BatchedEinsum& e, bool dry_r
 bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
   const BatchedEinsum& e = p.skel;
   const int n = e.n();
-  if (e.b() != 1 || n < 3 || n > 12 || p.complex_mode || p.functional || !p.tabs.empty()) {
-    *why = "path: one row of 3..12 plain real operands";
+  if (e.b() != 1 || n < 2 || n > 12 || p.complex_mode || p.functional || !p.tabs.empty()) {
+    *why = "path: one row of 2..12 plain real operands";
     return false;
   }
   // one element type: f64, or f32 (fp32 intermediates, like any fp32 chain)
@@ -1367,24 +1367,6 @@ bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
       return false;
     }
   const std::int64_t esize = est == ST_F32 ? 4 : 8;
-  // every index in at least two places (operands, output); none repeated in an operand
-  std::map<std::string, int> uses;
-  for (int k = 0; k < n; ++k) {
-    std::set<std::string> seen;
-    for (const auto& x : e.i_in[k]) {
-      if (!seen.insert(x).second) {
-        *why = "path: repeated index in an operand";
-        return false;
-      }
-      ++uses[x];
-    }
-  }
-  for (const auto& x : e.i_out) ++uses[x];
-  for (const auto& [x, c] : uses)
-    if (c < 2) {
-      *why = "path: index summed within one operand";
-      return false;
-    }
   const auto len = feinsum::index_lengths(e);
   std::vector<std::set<std::string>> idx(static_cast<size_t>(n));
   for (int k = 0; k < n; ++k) idx[static_cast<size_t>(k)].insert(e.i_in[k].begin(), e.i_in[k].end());
@@ -1421,7 +1403,15 @@ bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
     }
     cost[static_cast<size_t>(st)] = best;
   }
-  if (cost[static_cast<size_t>(full)] * 4.0 >= feinsum::flop_count(e)) {
+  // operands with private or repeated indices are first reduced to the
+  // indices they share (a one-operand step: sum / diagonal on the generic
+  // kernel); with two operands that is the only reason for a path
+  int pre = 0;
+  for (int k = 0; k < n; ++k)
+    if (keep[static_cast<size_t>(1) << k].size() != e.i_in[static_cast<size_t>(k)].size()) ++pre;
+  double pre_cost = 0;
+  for (int k = 0; k < n; ++k) pre_cost += size_of(idx[static_cast<size_t>(k)]);
+  if ((n == 2 && pre == 0) || (cost[static_cast<size_t>(full)] + pre_cost) * 4.0 >= feinsum::flop_count(e)) {
     *why = "path: no cheaper than the naive sum";
     return false;
   }
@@ -1438,43 +1428,59 @@ bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
   so.force_transform.clear();
   so.meta_override.clear();
   std::function<Opnd(int)> build = [&](int st) -> Opnd {
+    // a step over one or two operands into R (index list of st's keep set,
+    // or the einsum's output at the root)
+    auto make_step = [&](int s2, const std::vector<const Opnd*>& ops) {
+      Opnd R;
+      if (s2 == full) {
+        R.ix = e.i_out;
+      } else {
+        for (const Opnd* o : ops)
+          for (const auto& x : o->ix)
+            if (keep[static_cast<size_t>(s2)].count(x) && std::find(R.ix.begin(), R.ix.end(), x) == R.ix.end())
+              R.ix.push_back(x);
+      }
+      const int id = static_cast<int>(offs.size());
+      R.meta.name = "_path_t" + std::to_string(id);
+      R.meta.dtype = est == ST_F32 ? Dtype::float32 : Dtype::float64;
+      for (const auto& x : R.ix) R.meta.shape.push_back(len.at(x));
+      BatchedEinsum step;
+      step.i_out = R.ix;
+      step.args.emplace_back();
+      for (const Opnd* o : ops) {
+        step.i_in.push_back(o->ix);
+        step.args[0].push_back(o->meta);
+      }
+      PathStep ps;
+      ps.plan = make_plan(step, so);
+      for (const auto& L : ps.plan->leaves)
+        for (const Opnd* o : ops)
+          if (L.meta.name == o->meta.name) {
+            ps.src.push_back(o->src);
+            break;
+          }
+      if (s2 == full) {
+        ps.out = -1;
+        R.src = 0;
+      } else {
+        ps.out = id;
+        offs.push_back(bytes);
+        bytes += (R.meta.num_elements() * esize + 255) / 256 * 256;
+        R.src = -(1 + id);
+      }
+      steps.push_back(std::move(ps));
+      return R;
+    };
     if ((st & (st - 1)) == 0) {
       int k = 0;
       while (!(st >> k & 1)) ++k;
-      return Opnd{e.i_in[static_cast<size_t>(k)], e.args[0][static_cast<size_t>(k)], p.ops[static_cast<size_t>(k)].leaf};
+      Opnd leaf{e.i_in[static_cast<size_t>(k)], e.args[0][static_cast<size_t>(k)], p.ops[static_cast<size_t>(k)].leaf};
+      if (keep[static_cast<size_t>(st)].size() == leaf.ix.size() || st == full) return leaf;
+      return make_step(st, {&leaf});  // private / repeated indices reduced first
     }
     const int a = split[static_cast<size_t>(st)], b = st ^ a;
     const Opnd A = build(a), B = build(b);
-    Opnd R;
-    if (st == full) {
-      R.ix = e.i_out;
-    } else {
-      for (const auto* l : {&A.ix, &B.ix})
-        for (const auto& x : *l)
-          if (keep[static_cast<size_t>(st)].count(x) && std::find(R.ix.begin(), R.ix.end(), x) == R.ix.end()) R.ix.push_back(x);
-    }
-    const int id = static_cast<int>(offs.size());
-    R.meta.name = "_path_t" + std::to_string(id);
-    R.meta.dtype = est == ST_F32 ? Dtype::float32 : Dtype::float64;
-    for (const auto& x : R.ix) R.meta.shape.push_back(len.at(x));
-    BatchedEinsum step;
-    step.i_out = R.ix;
-    step.i_in = {A.ix, B.ix};
-    step.args = {{A.meta, B.meta}};
-    PathStep ps;
-    ps.plan = make_plan(step, so);
-    for (const auto& L : ps.plan->leaves) ps.src.push_back(L.meta.name == A.meta.name ? A.src : B.src);
-    if (st == full) {
-      ps.out = -1;
-      R.src = 0;
-    } else {
-      ps.out = id;
-      offs.push_back(bytes);
-      bytes += (R.meta.num_elements() * esize + 255) / 256 * 256;
-      R.src = -(1 + id);
-    }
-    steps.push_back(std::move(ps));
-    return R;
+    return make_step(st, {&A, &B});
   };
   try {
     build(full);

@@ -81,7 +81,8 @@ def test_default_plans_random(fe, ref, torch_cuda):
 
 def test_contraction_path(fe, ref, torch_cuda):
     """Three- and four-operand chains run as pairwise GETT / generic steps in
-    the optimal order; within the fp64 bar of the naive reference sum."""
+    the optimal order (operands with private indices reduced first); within
+    the fp64 bar of the naive reference sum."""
     m = lambda n, s: {"name": n, "shape": s, "dtype": "float64"}  # noqa: E731
     cases = [
         {"i_out": ["a", "d"], "i_in": [["a", "b"], ["b", "c"], ["c", "d"]],
@@ -90,6 +91,8 @@ def test_contraction_path(fe, ref, torch_cuda):
          "args": [[m("A", [30, 64]), m("B", [64, 24]), m("C", [24, 48]), m("D", [48, 36])]]},
         {"i_out": ["z", "a", "c"], "i_in": [["z", "a", "b"], ["b", "k"], ["z", "k", "c"]],
          "args": [[m("A", [3, 40, 64]), m("B", [64, 64]), m("C", [3, 64, 30])]]},
+        # two operands, one with a private index: reduced first, then GETT
+        {"i_out": ["a", "d"], "i_in": [["a", "x", "c"], ["c", "d"]], "args": [[m("A", [48, 6, 64]), m("B", [64, 40])]]},
     ]
     for k, e in enumerate(cases):
         plan = fe.Plan(einsum=e)

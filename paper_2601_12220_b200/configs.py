@@ -34,14 +34,14 @@ def fem_grad_permuted(E=10_000, b=3, NX=3, NI=10):
     return {"i_out": ["p", "k", "m"], "i_in": [["k", "n"], ["a", "p", "k"], ["a", "m", "n"]], "args": rows}
 
 
-def hex_poisson(E=2_000_000, b=8, P=5, ND=3, distinct=False):
+def hex_poisson(E=2_000_000, b=8, P=5, ND=3, distinct=False, dtype="float64"):
     """C2: sum-factorised P4 hex operator, 8 fields sharing G and A1..A3.
     distinct=True uses six different 1-D operators (F1..F3 forward, B1..B3
     backward) instead of A_d on both sides."""
-    A1, A2, A3 = _m("A1", (ND, P, P)), _m("A2", (ND, P, P)), _m("A3", (ND, P, P))
-    F1, F2, F3 = (_m(f"F{d}", (ND, P, P)) for d in (1, 2, 3)) if distinct else (A1, A2, A3)
-    G = _m("G", (ND, ND, E, P, P, P))
-    rows = [[A1, A2, A3, G, F1, F2, F3, _m(f"u{q + 1}", (E, P, P, P))] for q in range(b)]
+    A1, A2, A3 = (_m(f"A{d}", (ND, P, P), dtype) for d in (1, 2, 3))
+    F1, F2, F3 = (_m(f"F{d}", (ND, P, P), dtype) for d in (1, 2, 3)) if distinct else (A1, A2, A3)
+    G = _m("G", (ND, ND, E, P, P, P), dtype)
+    rows = [[A1, A2, A3, G, F1, F2, F3, _m(f"u{q + 1}", (E, P, P, P), dtype)] for q in range(b)]
     return {"i_out": ["e", "i", "m", "n"],
             "i_in": [["x", "a", "i"], ["x", "b", "m"], ["x", "c", "n"], ["x", "y", "e", "a", "b", "c"],
                      ["y", "a", "j"], ["y", "b", "k"], ["y", "c", "l"], ["e", "j", "k", "l"]],

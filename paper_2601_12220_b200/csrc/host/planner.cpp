@@ -1153,17 +1153,25 @@ bool bind_hex(Plan& p, std::string* why) {
   const int n = c.n();
   // pattern slot -> kernel matrix index: slots 0..2 backward (B1..B3), 4..6 forward (F1..F3)
   const int mat_of_slot[8] = {3, 4, 5, -1, 0, 1, 2, -1};
+  // one element type: f64, or f32 (the fp32 instance: four-element stages,
+  // so E % 4 == 0 below P = 6)
+  const int est = p.outputs[0].storage;
+  if ((est != ST_F64 && est != ST_F32) || (est == ST_F32 && h.P < 6 && h.E % 4 != 0)) {
+    *why = "storage other than uniform f64 / f32 (f32: E % 4 == 0)";
+    return false;
+  }
+  h.f32 = est == ST_F32;
   for (int q = 0; q < c.b(); ++q) {
     const int ur = p.canon.sigma_row[q];
     auto leaf_at = [&](int role) -> int {
       const OperandStatic& op = p.ops[static_cast<size_t>(ur) * n + p.canon.sigma_slot[m->slot[role]]];
-      if (op.kind != OPK_PLAIN || leaf_info(p, op.leaf).storage != ST_F64) return -1;
+      if (op.kind != OPK_PLAIN || leaf_info(p, op.leaf).storage != est) return -1;
       return op.leaf;
     };
     for (int role = 0; role < 8; ++role) {
       const int leaf = leaf_at(role);
       if (leaf < 0) {
-        *why = "functional or non-f64 operand";
+        *why = "functional operand or mixed storage";
         return false;
       }
       if (role == 7) {
@@ -1183,8 +1191,8 @@ bool bind_hex(Plan& p, std::string* why) {
         slot = leaf;
       }
     }
-    if (p.outputs[ur].storage != ST_F64) {
-      *why = "non-f64 output";
+    if (p.outputs[ur].storage != est) {
+      *why = "mixed output storage";
       return false;
     }
     h.out_row.push_back(ur);
@@ -1976,6 +1984,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
       L.P = h.P;
       L.rows = static_cast<int>(h.u.size());
       L.variant = meta_int(plan.meta, "v", 2);
+      L.f32 = h.f32;
       L.ne = meta_int(plan.meta, "ne", 4);
       for (int k = 0; k < 6; ++k) L.mats[k] = static_cast<const double*>(d_in[h.mats[k]]);
       L.G = static_cast<const double*>(d_in[h.g]);

@@ -120,6 +120,7 @@ struct HexBinding {
   int mats[6] = {-1, -1, -1, -1, -1, -1};  // leaf of F1 F2 F3 B1 B2 B3
   int g = -1;
   std::vector<int> u, out_row;  // per canonical row
+  bool f32 = false;             // every array float32 (fp32 instance of the v2 kernel)
 };
 
 struct Plan;

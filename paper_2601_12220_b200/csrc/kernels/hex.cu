@@ -304,6 +304,7 @@ constexpr int kMaxQ = 6;
 // F1 F2 F3 B1 B2 B3 packed as stored: matrix k, direction d, entry (o, i) at
 // (k * ND + d) * Q^2 + o * Q + i (one copy per matrix per launch)
 __constant__ double c_hex_ops[6 * ND * kMaxQ * kMaxQ];
+__constant__ float c_hex_ops_f[6 * ND * kMaxQ * kMaxQ];  // the fp32 instance's copy
 
 template <int Q>
 struct Hx {
@@ -321,22 +322,26 @@ struct Hex2Dev {
 };
 
 // forward operator entry M[o][i] = F[o][i]; backward M[o][i] = B[i][o]
-template <int Q, int K, int D, bool kBack>
-__device__ __forceinline__ double cop(int o, int i) {
+template <typename T, int Q, int K, int D, bool kBack>
+__device__ __forceinline__ T cop(int o, int i) {
   constexpr int base = (K * ND + D) * Q * Q;
-  return kBack ? c_hex_ops[base + i * Q + o] : c_hex_ops[base + o * Q + i];
+  const int at = kBack ? base + i * Q + o : base + o * Q + i;
+  if constexpr (sizeof(T) == 4)
+    return c_hex_ops_f[at];
+  else
+    return c_hex_ops[at];
 }
 
-template <int Q, int K, int D, bool kBack>
-__device__ __forceinline__ void rows_c(double (&v)[Q][Q]) {
+template <typename T, int Q, int K, int D, bool kBack>
+__device__ __forceinline__ void rows_c(T (&v)[Q][Q]) {
 #pragma unroll
   for (int r = 0; r < Q; ++r) {
-    double o[Q];
+    T o[Q];
 #pragma unroll
     for (int a = 0; a < Q; ++a) {
-      double s = cop<Q, K, D, kBack>(a, 0) * v[r][0];
+      T s = cop<T, Q, K, D, kBack>(a, 0) * v[r][0];
 #pragma unroll
-      for (int b = 1; b < Q; ++b) s = fma(cop<Q, K, D, kBack>(a, b), v[r][b], s);
+      for (int b = 1; b < Q; ++b) s = fma(cop<T, Q, K, D, kBack>(a, b), v[r][b], s);
       o[a] = s;
     }
 #pragma unroll
@@ -344,16 +349,16 @@ __device__ __forceinline__ void rows_c(double (&v)[Q][Q]) {
   }
 }
 
-template <int Q, int K, int D, bool kBack>
-__device__ __forceinline__ void cols_c(double (&v)[Q][Q]) {
+template <typename T, int Q, int K, int D, bool kBack>
+__device__ __forceinline__ void cols_c(T (&v)[Q][Q]) {
 #pragma unroll
   for (int col = 0; col < Q; ++col) {
-    double o[Q];
+    T o[Q];
 #pragma unroll
     for (int a = 0; a < Q; ++a) {
-      double s = cop<Q, K, D, kBack>(a, 0) * v[0][col];
+      T s = cop<T, Q, K, D, kBack>(a, 0) * v[0][col];
 #pragma unroll
-      for (int b = 1; b < Q; ++b) s = fma(cop<Q, K, D, kBack>(a, b), v[b][col], s);
+      for (int b = 1; b < Q; ++b) s = fma(cop<T, Q, K, D, kBack>(a, b), v[b][col], s);
       o[a] = s;
     }
 #pragma unroll
@@ -362,15 +367,15 @@ __device__ __forceinline__ void cols_c(double (&v)[Q][Q]) {
 }
 
 // pass A: u plane j -> t_y plane j (F3[y] along l, F2[y] along k)
-template <int Q, int Y>
-__device__ __forceinline__ void pass_a(const double* in, double* out) {
-  double v[Q][Q];
+template <typename T, int Q, int Y>
+__device__ __forceinline__ void pass_a(const T* in, T* out) {
+  T v[Q][Q];
 #pragma unroll
   for (int k = 0; k < Q; ++k)
 #pragma unroll
     for (int l = 0; l < Q; ++l) v[k][l] = in[k * Q + l];
-  rows_c<Q, 2, Y, false>(v);
-  cols_c<Q, 1, Y, false>(v);
+  rows_c<T, Q, 2, Y, false>(v);
+  cols_c<T, Q, 1, Y, false>(v);
 #pragma unroll
   for (int b = 0; b < Q; ++b)
 #pragma unroll
@@ -378,15 +383,15 @@ __device__ __forceinline__ void pass_a(const double* in, double* out) {
 }
 
 // pass C: q'_x plane i -> partial y_x plane i (B2[x]^T along b, B3[x]^T along c)
-template <int Q, int X>
-__device__ __forceinline__ void pass_c(double* io) {
-  double v[Q][Q];
+template <typename T, int Q, int X>
+__device__ __forceinline__ void pass_c(T* io) {
+  T v[Q][Q];
 #pragma unroll
   for (int b = 0; b < Q; ++b)
 #pragma unroll
     for (int c = 0; c < Q; ++c) v[b][c] = io[b * Q + c];
-  cols_c<Q, 4, X, true>(v);
-  rows_c<Q, 5, X, true>(v);
+  cols_c<T, Q, 4, X, true>(v);
+  rows_c<T, Q, 5, X, true>(v);
 #pragma unroll
   for (int m = 0; m < Q; ++m)
 #pragma unroll
@@ -401,15 +406,15 @@ __device__ __forceinline__ void pass_c(double* io) {
 // Chain barriers b0 (x = 0 -> 1) and b0 + 1 (x = 1 -> 2); every lane of the
 // warp takes part (bar is warp-aligned), lanes without a task compute on
 // zeros and store nothing.
-template <int Q, int X>
-__device__ __forceinline__ void pass_c_sum(const double* in, double* ys, int b0, bool active) {
-  double v[Q][Q];
+template <typename T, int Q, int X>
+__device__ __forceinline__ void pass_c_sum(const T* in, T* ys, int b0, bool active) {
+  T v[Q][Q];
 #pragma unroll
   for (int b = 0; b < Q; ++b)
 #pragma unroll
     for (int c = 0; c < Q; ++c) v[b][c] = active ? in[b * Q + c] : 0.0;
-  cols_c<Q, 4, X, true>(v);
-  rows_c<Q, 5, X, true>(v);
+  cols_c<T, Q, 4, X, true>(v);
+  rows_c<T, Q, 5, X, true>(v);
   if constexpr (X > 0) asm volatile("bar.sync %0, 64;" ::"r"(b0 + X - 1) : "memory");
   if (active) {
 #pragma unroll
@@ -421,14 +426,14 @@ __device__ __forceinline__ void pass_c_sum(const double* in, double* ys, int b0,
 }
 
 // F1[y] along j on one line (y compile-time)
-template <int Q, int Y>
-__device__ __forceinline__ void line_f1(double (&t)[Q]) {
-  double o[Q];
+template <typename T, int Q, int Y>
+__device__ __forceinline__ void line_f1(T (&t)[Q]) {
+  T o[Q];
 #pragma unroll
   for (int a = 0; a < Q; ++a) {
-    double s = cop<Q, 0, Y, false>(a, 0) * t[0];
+    T s = cop<T, Q, 0, Y, false>(a, 0) * t[0];
 #pragma unroll
-    for (int j = 1; j < Q; ++j) s = fma(cop<Q, 0, Y, false>(a, j), t[j], s);
+    for (int j = 1; j < Q; ++j) s = fma(cop<T, Q, 0, Y, false>(a, j), t[j], s);
     o[a] = s;
   }
 #pragma unroll
@@ -436,23 +441,23 @@ __device__ __forceinline__ void line_f1(double (&t)[Q]) {
 }
 
 // B1[x]^T along a on one line, stored with stride Q^2
-template <int Q, int X>
-__device__ __forceinline__ void line_b1(const double (&t)[Q], double* out) {
+template <typename T, int Q, int X>
+__device__ __forceinline__ void line_b1(const T (&t)[Q], T* out) {
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    double s = cop<Q, 3, X, true>(i, 0) * t[0];
+    T s = cop<T, Q, 3, X, true>(i, 0) * t[0];
 #pragma unroll
-    for (int a = 1; a < Q; ++a) s = fma(cop<Q, 3, X, true>(i, a), t[a], s);
+    for (int a = 1; a < Q; ++a) s = fma(cop<T, Q, 3, X, true>(i, a), t[a], s);
     out[i * Hx<Q>::Q2] = s;
   }
 }
 
 // pass B on line (k,l) of NF fields: wl[f] = W + cube*CS + kl (direction 0),
 // direction stride ds; g = Gs + el*Q3 + kl with (x,y) block stride gs
-template <int Q, int NF>
-__device__ __forceinline__ void pass_b(double* const (&wl)[NF], int ds, const double* g, int gs) {
+template <typename T, int Q, int NF>
+__device__ __forceinline__ void pass_b(T* const (&wl)[NF], int ds, const T* g, int gs) {
   constexpr int Q2 = Hx<Q>::Q2;
-  double t[NF][ND][Q];
+  T t[NF][ND][Q];
 #pragma unroll
   for (int f = 0; f < NF; ++f)
 #pragma unroll
@@ -461,24 +466,24 @@ __device__ __forceinline__ void pass_b(double* const (&wl)[NF], int ds, const do
       for (int j = 0; j < Q; ++j) t[f][y][j] = wl[f][y * ds + j * Q2];
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
-    line_f1<Q, 0>(t[f][0]);
-    line_f1<Q, 1>(t[f][1]);
-    line_f1<Q, 2>(t[f][2]);
+    line_f1<T, Q, 0>(t[f][0]);
+    line_f1<T, Q, 1>(t[f][1]);
+    line_f1<T, Q, 2>(t[f][2]);
   }
   // q_x = sum_y G[x,y] t_y, pointwise; G read once for all NF fields
 #pragma unroll
   for (int a = 0; a < Q; ++a) {
-    double gv[ND][ND];
+    T gv[ND][ND];
 #pragma unroll
     for (int x = 0; x < ND; ++x)
 #pragma unroll
       for (int y = 0; y < ND; ++y) gv[x][y] = g[(x * ND + y) * gs + a * Q2];
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-      double q[ND];
+      T q[ND];
 #pragma unroll
       for (int x = 0; x < ND; ++x) {
-        double s = gv[x][0] * t[f][0][a];
+        T s = gv[x][0] * t[f][0][a];
         s = fma(gv[x][1], t[f][1][a], s);
         q[x] = fma(gv[x][2], t[f][2][a], s);
       }
@@ -488,9 +493,9 @@ __device__ __forceinline__ void pass_b(double* const (&wl)[NF], int ds, const do
   }
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
-    line_b1<Q, 0>(t[f][0], wl[f]);
-    line_b1<Q, 1>(t[f][1], wl[f] + ds);
-    line_b1<Q, 2>(t[f][2], wl[f] + 2 * ds);
+    line_b1<T, Q, 0>(t[f][0], wl[f]);
+    line_b1<T, Q, 1>(t[f][1], wl[f] + ds);
+    line_b1<T, Q, 2>(t[f][2], wl[f] + 2 * ds);
   }
 }
 
@@ -503,21 +508,23 @@ struct HexCfg {
   static constexpr int kThreads = (kTasks + 31) / 32 * 32 + 32;
 };
 
-template <int Q, int NE2>
+template <typename T, int Q, int NE2>
 __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const __grid_constant__ Hex2Dev p) {
   constexpr int NE = NE2;
   constexpr int Q2 = Hx<Q>::Q2, Q3 = Hx<Q>::Q3, CS = Hx<Q>::CS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sm = reinterpret_cast<double*>(smem_raw);
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  const T* const pG = reinterpret_cast<const T*>(p.G);
   const int R = p.rows;
   const int nblk = NE * R;   // cubes per stage, cube = field * NE + element
   const int ds = nblk * CS;  // direction stride in W
   // layout (doubles): Gs[9][NE*Q3] | Us[R][NE*Q3] | W[ND][nblk][CS] | Ys[R][NE*Q3] | mbar {G, U}
-  double* Gs = sm;
-  double* Us = Gs + ND * ND * NE * Q3;
-  double* W = Us + R * NE * Q3;
-  double* Ys = W + ND * ds;  // output staging: one bulk store per field and stage
-  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(Ys + R * NE * Q3);
+  T* Gs = sm;
+  T* Us = Gs + ND * ND * NE * Q3;
+  T* W = Us + R * NE * Q3;
+  T* Ys = W + ND * ds;  // output staging: one bulk store per field and stage
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(
+      (reinterpret_cast<std::uintptr_t>(Ys + R * NE * Q3) + 7) & ~std::uintptr_t{7});
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar[0], 1);
     ptx::mbar_init(&bar[1], 1);
@@ -526,17 +533,17 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
   __syncthreads();
 
   const std::int64_t nstages = p.E / NE;
-  const std::uint32_t bytes = static_cast<std::uint32_t>(NE * Q3 * 8);
+  const std::uint32_t bytes = static_cast<std::uint32_t>(NE * Q3 * sizeof(T));
   auto issue_g = [&](std::int64_t st) {
     ptx::mbar_arrive_expect_tx(&bar[0], bytes * static_cast<std::uint32_t>(ND * ND));
     const std::int64_t e0 = st * NE;
     for (int xy = 0; xy < ND * ND; ++xy)
-      ptx::bulk_g2s(Gs + xy * NE * Q3, p.G + (xy * p.E + e0) * Q3, bytes, &bar[0]);
+      ptx::bulk_g2s(Gs + xy * NE * Q3, pG + (xy * p.E + e0) * Q3, bytes, &bar[0]);
   };
   auto issue_u = [&](std::int64_t st) {
     ptx::mbar_arrive_expect_tx(&bar[1], bytes * static_cast<std::uint32_t>(R));
     const std::int64_t e0 = st * NE;
-    for (int f = 0; f < R; ++f) ptx::bulk_g2s(Us + f * NE * Q3, p.U[f] + e0 * Q3, bytes, &bar[1]);
+    for (int f = 0; f < R; ++f) ptx::bulk_g2s(Us + f * NE * Q3, reinterpret_cast<const T*>(p.U[f]) + e0 * Q3, bytes, &bar[1]);
   };
   // the copy engine is driven by lane 0 of the last warp, which has no work in
   // passes A / C and none in B at the pinned config, so issuing the next
@@ -552,8 +559,8 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
   const int ptask = threadIdx.x - dir * nblk * Q;
   const bool pactive = dir < ND && threadIdx.x < blockDim.x - 32;
   const int pplane = ptask / nblk, pcube = ptask - pplane * nblk;  // cube fastest
-  const double* a_in = Us + pcube * Q3 + pplane * Q2;
-  double* a_out = W + dir * ds + pcube * CS + pplane * Q2;
+  const T* a_in = Us + pcube * Q3 + pplane * Q2;
+  T* a_out = W + dir * ds + pcube * CS + pplane * Q2;
   // pass B: thread -> (line, element, field pair (f, f + H)), line fastest
   const int H = (R + 1) / 2;
   const int nbt = H * NE * Q2;
@@ -567,9 +574,9 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
 
     ptx::mbar_wait(&bar[1], phase);
     if (pactive) {
-      if (dir == 0) pass_a<Q, 0>(a_in, a_out);
-      else if (dir == 1) pass_a<Q, 1>(a_in, a_out);
-      else pass_a<Q, 2>(a_in, a_out);
+      if (dir == 0) pass_a<T, Q, 0>(a_in, a_out);
+      else if (dir == 1) pass_a<T, Q, 1>(a_in, a_out);
+      else pass_a<T, Q, 2>(a_in, a_out);
     }
     __syncthreads();
     if (producer && more) issue_u(st + gridDim.x);
@@ -579,12 +586,12 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
       const int kl = t % Q2;
       const int r = t / Q2;
       const int el = r % NE, f0 = r / NE, f1 = f0 + H;
-      const double* g = Gs + el * Q3 + kl;
+      const T* g = Gs + el * Q3 + kl;
       // odd R: the last thread pairs its field with itself (same values
       // written twice by the same thread) — one code path, smaller kernel
-      double* const w0 = W + (f0 * NE + el) * CS + kl;
-      double* const wl[2] = {w0, f1 < R ? W + (f1 * NE + el) * CS + kl : w0};
-      pass_b<Q, 2>(wl, ds, g, NE * Q3);
+      T* const w0 = W + (f0 * NE + el) * CS + kl;
+      T* const wl[2] = {w0, f1 < R ? W + (f1 * NE + el) * CS + kl : w0};
+      pass_b<T, Q, 2>(wl, ds, g, NE * Q3);
     }
     if (producer) ptx::bulk_wait_read<0>();  // the previous stage's stores have read Ys
     __syncthreads();
@@ -593,23 +600,23 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
     const std::int64_t e0 = st * NE;
     if (fused) {
       if (pactive) {
-        double* ys = Ys + pcube * Q3 + pplane * Q2;  // cube * Q3 = field * NE * Q3 + element * Q3
-        if (dir == 0) pass_c_sum<Q, 0>(a_out, ys, 1 + 2 * pplane, true);
-        else if (dir == 1) pass_c_sum<Q, 1>(a_out, ys, 1 + 2 * pplane, true);
-        else pass_c_sum<Q, 2>(a_out, ys, 1 + 2 * pplane, true);
+        T* ys = Ys + pcube * Q3 + pplane * Q2;  // cube * Q3 = field * NE * Q3 + element * Q3
+        if (dir == 0) pass_c_sum<T, Q, 0>(a_out, ys, 1 + 2 * pplane, true);
+        else if (dir == 1) pass_c_sum<T, Q, 1>(a_out, ys, 1 + 2 * pplane, true);
+        else pass_c_sum<T, Q, 2>(a_out, ys, 1 + 2 * pplane, true);
       }
       ptx::fence_proxy_async();
       __syncthreads();  // W is rewritten by the next stage's pass A; Ys complete
       if (producer) {
-        for (int f = 0; f < R; ++f) ptx::bulk_s2g(p.Y[f] + e0 * Q3, Ys + f * NE * Q3, bytes);
+        for (int f = 0; f < R; ++f) ptx::bulk_s2g(reinterpret_cast<T*>(p.Y[f]) + e0 * Q3, Ys + f * NE * Q3, bytes);
         ptx::bulk_commit();
       }
       continue;
     }
     if (pactive) {
-      if (dir == 0) pass_c<Q, 0>(a_out);
-      else if (dir == 1) pass_c<Q, 1>(a_out);
-      else pass_c<Q, 2>(a_out);
+      if (dir == 0) pass_c<T, Q, 0>(a_out);
+      else if (dir == 1) pass_c<T, Q, 1>(a_out);
+      else pass_c<T, Q, 2>(a_out);
     }
     __syncthreads();
 
@@ -619,7 +626,7 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
     // instead of a burst of global stores at the end of every stage
     for (int off = threadIdx.x; off < NE * Q3; off += blockDim.x) {
       const int el = off / Q3;
-      const double* w = W + el * CS + (off - el * Q3);
+      const T* w = W + el * CS + (off - el * Q3);
 #pragma unroll
       for (int f = 0; f < kMaxFields; ++f)
         if (f < R) Ys[f * NE * Q3 + off] = (w[f * NE * CS] + w[ds + f * NE * CS]) + w[2 * ds + f * NE * CS];
@@ -627,7 +634,7 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
     ptx::fence_proxy_async();
     __syncthreads();  // W is rewritten by the next stage's pass A; Ys complete
     if (producer) {
-      for (int f = 0; f < R; ++f) ptx::bulk_s2g(p.Y[f] + e0 * Q3, Ys + f * NE * Q3, bytes);
+      for (int f = 0; f < R; ++f) ptx::bulk_s2g(reinterpret_cast<T*>(p.Y[f]) + e0 * Q3, Ys + f * NE * Q3, bytes);
       ptx::bulk_commit();
     }
   }
@@ -644,19 +651,21 @@ struct HexConstSlot {
 struct Mats6 {
   const double* m[6];
 };
-__global__ void gather_ops(const __grid_constant__ Mats6 src, int n, double* dst) {
-  for (int t = threadIdx.x; t < 6 * n; t += blockDim.x) dst[t] = src.m[t / n][t % n];
+template <typename T>
+__global__ void gather_ops(const __grid_constant__ Mats6 src, int n, T* dst) {
+  for (int t = threadIdx.x; t < 6 * n; t += blockDim.x)
+    dst[t] = static_cast<T>(reinterpret_cast<const T*>(src.m[t / n])[t % n]);
 }
 std::mutex g_hex_mu;
 HexConstSlot g_hex_slot[64];
 
-template <int Q, int NE2>
+template <typename T, int Q, int NE2>
 int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
   constexpr int Q2 = Hx<Q>::Q2, Q3 = Hx<Q>::Q3, CS = Hx<Q>::CS;
   const int R = L.rows;
   const int nblk = NE2 * R;
   constexpr int threads = HexCfg<Q, NE2>::kThreads;
-  auto kern = hex2_kernel<Q, NE2>;
+  auto kern = hex2_kernel<T, Q, NE2>;
   Hex2Dev d{};
   d.E = L.E;
   d.rows = R;
@@ -666,7 +675,7 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
     d.Y[f] = L.Y[f];
   }
   const size_t doubles = ND * ND * NE2 * Q3 + 2 * R * NE2 * Q3 + ND * nblk * CS;
-  const size_t smem = doubles * 8 + 16;
+  const size_t smem = doubles * sizeof(T) + 24;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -688,8 +697,11 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
   if (!slot.stage && (e = cudaMalloc(&slot.stage, 6 * ND * kMaxQ * kMaxQ * sizeof(double))) != cudaSuccess) return e;
   Mats6 m6{};
   for (int k = 0; k < 6; ++k) m6.m[k] = L.mats[k];
-  gather_ops<<<1, 256, 0, st>>>(m6, ND * Q2, slot.stage);
-  e = cudaMemcpyToSymbolAsync(c_hex_ops, slot.stage, 6 * ND * Q2 * sizeof(double), 0, cudaMemcpyDeviceToDevice, st);
+  gather_ops<T><<<1, 256, 0, st>>>(m6, ND * Q2, reinterpret_cast<T*>(slot.stage));
+  if constexpr (sizeof(T) == 4)
+    e = cudaMemcpyToSymbolAsync(c_hex_ops_f, slot.stage, 6 * ND * Q2 * sizeof(T), 0, cudaMemcpyDeviceToDevice, st);
+  else
+    e = cudaMemcpyToSymbolAsync(c_hex_ops, slot.stage, 6 * ND * Q2 * sizeof(T), 0, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return e;
   kern<<<static_cast<int>(grid), threads, smem, st>>>(d);
   e = cudaGetLastError();
@@ -701,10 +713,19 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
 // (shared memory)
 template <int Q>
 int launch_hex2_q(const HexLaunch& L, cudaStream_t st) {
-  if constexpr (Q < 6) {
-    if (L.ne != 2 && L.E % 4 == 0) return launch_hex2_t<Q, 4>(L, st);
+  if (L.f32) {
+    // fp32: four-element stages (16-byte bulk-copy runs), two at Q = 6
+    if constexpr (Q < 6) {
+      if (L.E % 4 != 0) return cudaErrorInvalidValue;
+      return launch_hex2_t<float, Q, 4>(L, st);
+    } else {
+      return launch_hex2_t<float, Q, 2>(L, st);
+    }
   }
-  return launch_hex2_t<Q, 2>(L, st);
+  if constexpr (Q < 6) {
+    if (L.ne != 2 && L.E % 4 == 0) return launch_hex2_t<double, Q, 4>(L, st);
+  }
+  return launch_hex2_t<double, Q, 2>(L, st);
 }
 
 int launch_hex2(const HexLaunch& L, cudaStream_t st) {
@@ -727,7 +748,7 @@ bool hex_supported(int nd, int p, std::int64_t E, int rows) {
 int launch_hex(const HexLaunch& L, void* stream) {
   if (!hex_supported(L.ND, L.P, L.E, L.rows)) return cudaErrorInvalidValue;
   if (L.E == 0) return cudaSuccess;
-  if (L.variant != 1 || L.P != P) return launch_hex2(L, static_cast<cudaStream_t>(stream));
+  if (L.variant != 1 || L.P != P || L.f32) return launch_hex2(L, static_cast<cudaStream_t>(stream));
   HexDev d{};
   d.E = L.E;
   d.rows = L.rows;

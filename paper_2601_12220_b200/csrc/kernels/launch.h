@@ -256,6 +256,7 @@ struct HexLaunch {
   double* Y[8];
   int variant;  // 2: constant-bank operators, plane/line passes (default); 1: register-plane passes
   int ne;       // v2 elements per stage: 4 (default when E % 4 == 0) or 2
+  bool f32;     // every array float (pointers reinterpreted; v2 only, E % 4 == 0 below Q = 6)
 };
 
 int launch_hex(const HexLaunch& p, void* stream);

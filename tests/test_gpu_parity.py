@@ -598,6 +598,20 @@ def test_hex_sumfact_small(fe, ref, torch_cuda, meta):
             assert rel_err(g, w) <= FP64_TOL, (E, b)
 
 
+def test_hex_sumfact_fp32(fe, ref, torch_cuda):
+    """float32 arrays take the fp32 instance of the v2 hex kernel (FFMA,
+    half the bytes), within the fp32 bar of the reference."""
+    from paper_2601_12220_b200 import configs as C
+    for E, b, distinct, P in [(4, 1, False, 5), (8, 8, True, 5), (4, 3, True, 4), (6, 2, False, 6)]:
+        e = C.hex_poisson(E=E, b=b, distinct=distinct, P=P, dtype="float32")
+        plan = fe.Plan(einsum=e)
+        assert plan.info["transform"] == "hex_sumfact/v1", plan.info
+        bind = ref.random_bindings(e, E + b + P)
+        want = ref.evaluate(e, bind)
+        for g, w in zip(run_plan(torch_cuda, plan, bind), want):
+            assert g.dtype == np.float32 and rel_err(g, w.real) <= 1e-5, (E, b, P)
+
+
 def test_hex_sumfact_large_sampled(fe, torch_cuda):
     """E = 200k elements, 8 fields (the C2 grid shape), checked on sampled
     elements against an independent fp64 torch evaluation of the same einsum."""

@@ -7,6 +7,7 @@ traffic.json (per-config DRAM bytes of the dominant kernel, read by bench.py).
 import json
 import os
 import re
+import shutil
 import subprocess
 import sys
 
@@ -18,6 +19,7 @@ go = os.path.join(ROOT, "gpurun_out")
 
 launches = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_summary.py"), os.path.join(go, "launches.csv")],
                           capture_output=True, text=True).stdout
+shutil.copy(os.path.join(go, "launches.csv"), os.path.join(out, "launches.csv"))  # the raw list the summary is from
 with open(os.path.join(out, "launches_summary.txt"), "w") as f:
     f.write("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised) over\n"
             "python bench.py --configs C1,C2,C3,C4-f64,C4-f32,C5 --steps 2 --warmup 1 (incl. data fill + L2 flush kernels)\n\n")

@@ -79,6 +79,44 @@ def test_default_plans_random(fe, ref, torch_cuda):
     assert "generic/v1" in picked
 
 
+def _random_gett_einsum(rng):
+    """A random 2-operand contraction: M / N / K groups of 1-2 indices, an
+    optional batch index, random index orders in A, B and C."""
+    letters = iter("abcdefghij")
+    def group(n, big):
+        g = [(next(letters), big if k == 0 else int(rng.choice([2, 3]))) for k in range(n)]
+        return g
+    M = group(int(rng.integers(1, 3)), int(rng.choice([24, 32])))
+    N = group(int(rng.integers(1, 3)), int(rng.choice([24, 32])))
+    K = group(int(rng.integers(1, 3)), 64)
+    Z = group(int(rng.integers(0, 2)), 3)
+    ext = dict(M + N + K + Z)
+    def order(*gs):
+        xs = [x for g in gs for x, _ in g]
+        rng.shuffle(xs)
+        return xs
+    a, b, c = order(M, K, Z), order(K, N, Z), order(Z, M, N)
+    m = lambda n, ix: {"name": n, "shape": [ext[x] for x in ix], "dtype": "float64"}  # noqa: E731
+    return {"i_out": c, "i_in": [a, b], "args": [[m("A", a), m("B", b)]]}
+
+
+def test_gett_random_two_operand(fe, ref, torch_cuda):
+    """Random two-operand contractions (groups of one or two indices, random
+    orders, optional batch index): whatever the planner picks matches the
+    reference exactly on dyadic data, and most of them take the GETT kernel
+    (split / folded / repacked / batched forms)."""
+    rng = np.random.default_rng(5)
+    taken = 0
+    for k in range(24):
+        e = _random_gett_einsum(rng)
+        b = ref.random_bindings(e, 100 + k)
+        plan = fe.Plan(einsum=e)
+        taken += plan.info["transform"] == "gett_dmma/v1"
+        got = run_plan(torch_cuda, plan, b)[0]
+        assert np.array_equal(got, ref.evaluate(e, b)[0].real), (k, e, plan.info["transform"])
+    assert taken >= 12, taken
+
+
 def test_contraction_path(fe, ref, torch_cuda):
     """Three- and four-operand chains run as pairwise GETT / generic steps in
     the optimal order (operands with private indices reduced first); within

@@ -1686,6 +1686,25 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
       cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_pack_b),
                             sizeof(double) * static_cast<size_t>(g.ext_no * g.ext_ni * g.ext_ka * g.ext_kb * g.nz)),
                  "cudaMalloc(gett packed B)");
+    // split K when the output has too few 144 x 144 tiles to fill the SMs
+    // (matmul 512^3: 16 tiles) — slices of the k steps run as separate tiles
+    // and a second pass sums them in slice order (fact meta ks=N forces)
+    {
+      GettBinding& gm = p.gett;
+      const std::int64_t tiles = (gm.ext_mo + 1) / 2 * ((gm.ext_no + 1) / 2) * gm.nz;
+      const std::int64_t ksteps = (gm.ext_ka + 7) / 8 * ((gm.ext_kb + 3) / 4);
+      const std::int64_t csize = gm.ext_mo * gm.ext_mi * gm.ext_no * gm.ext_ni * gm.nz;
+      std::int64_t ks = 1;
+      if (tiles * 2 <= p.sm_count) ks = std::min<std::int64_t>({16, p.sm_count / tiles, ksteps / 2});
+      ks = meta_int(p.meta, "ks", static_cast<int>(ks));
+      bool affine = false;
+      for (const auto& r : gm.rows) affine = affine || r.a_alpha >= 0 || r.b_alpha >= 0;
+      if (ks >= 2 && !affine && ks * csize <= (std::int64_t{1} << 27)) {
+        gm.ksplit = static_cast<int>(ks);
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_ws), sizeof(double) * static_cast<size_t>(ks * csize)),
+                   "cudaMalloc(gett split-K workspace)");
+      }
+    }
     if (g.c_f32)
       cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.d_cbuf),
                             sizeof(double) * static_cast<size_t>(g.ext_mo * g.ext_mi * g.ext_no * g.ext_ni * g.nz)),
@@ -1709,6 +1728,7 @@ Plan::~Plan() {
   if (d_pack_a) cudaFree(d_pack_a);
   if (d_pack_b) cudaFree(d_pack_b);
   if (d_cbuf) cudaFree(d_cbuf);
+  if (d_ws) cudaFree(d_ws);
   if (d_tab) cudaFree(d_tab);
   if (d_inter) cudaFree(d_inter);
 }
@@ -1955,6 +1975,8 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         L.a_z = b.a_z;
         L.b_z = b.b_z;
         L.c_z = b.c_z;
+        L.ksplit = b.ksplit;
+        L.ws = plan.d_ws;
         L.a_alpha = r.a_alpha;
         L.a_beta = r.a_beta;
         L.b_alpha = r.b_alpha;

@@ -94,6 +94,7 @@ struct GettBinding {
   // a_z / b_z (after a repack: the packed block size), source strides for
   // the repack, C stride
   std::int64_t nz = 1, a_z = 0, b_z = 0, a_z_src = 0, b_z_src = 0, c_z = 0;
+  int ksplit = 1;  // split-K slices for small tile counts (plan workspace d_ws)
   std::int64_t a_src[4] = {0, 0, 0, 0}, b_src[4] = {0, 0, 0, 0};
   struct Row {
     int a_leaf, b_leaf, out_row;
@@ -194,6 +195,7 @@ struct Plan {
   double* d_pack_a = nullptr;   // GETT repacked operands (see GettBinding)
   double* d_pack_b = nullptr;
   double* d_cbuf = nullptr;     // GETT f64 result staging for fp32 outputs
+  double* d_ws = nullptr;       // GETT split-K partial tiles
   GenericLaunch gen{};  // pointers filled per execution
   int sm_count = 148;
 

@@ -65,6 +65,11 @@ struct GettDev {
   double kdim;         // |K| = ext_ka * ext_kb
   int stages, group;  // group: side of the square raster block (tiles sharing A/B slices in L2)
   std::int64_t nz, c_z;  // batch count (an index of A, B and C) and its C stride; 5-D maps when nz > 1
+  // split K: ksplit slices of the k steps, slice s writes its partial tile
+  // into ws + s * csize (C's strides); a reduce pass sums the slices into C
+  int ksplit;
+  double* ws;
+  std::int64_t csize;
 };
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1,
@@ -98,8 +103,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::int64_t per_z = p.mo * p.no;  // tiles per batch value
-  const std::int64_t ntiles = per_z * p.nz;
-  const std::int64_t ksteps = p.ka_steps * p.kb_steps;
+  const std::int64_t per_s = per_z * p.nz;  // tiles per K slice
+  const std::int64_t ntiles = per_s * p.ksplit;
+  const std::int64_t ksteps_all = p.ka_steps * p.kb_steps;
+  // k steps [k_lo(s), k_lo(s + 1)) of slice s
+  auto k_lo = [&](std::int64_t s) { return ksteps_all * s / p.ksplit; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -133,9 +141,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     std::int64_t it = 0;
     for (std::int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       std::int64_t mo, no;
-      const int z = static_cast<int>(t / per_z);
-      tile_coords(t - z * per_z, mo, no);
-      for (std::int64_t ks = 0; ks < ksteps; ++ks, ++it) {
+      const std::int64_t sl = t / per_s, tz = t - sl * per_s;
+      const int z = static_cast<int>(tz / per_z);
+      tile_coords(tz - z * per_z, mo, no);
+      for (std::int64_t ks = k_lo(sl); ks < k_lo(sl + 1); ++ks, ++it) {
         const int s = static_cast<int>(it % S);
         const std::uint32_t round = static_cast<std::uint32_t>(it / S);
         ptx::mbar_wait(&empty[s], (round & 1u) ^ 1u);
@@ -181,15 +190,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::int64_t it = 0;
   for (std::int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     std::int64_t mo, no;
-    const std::int64_t z = t / per_z;
-    tile_coords(t - z * per_z, mo, no);
+    const std::int64_t sl = t / per_s, tz = t - sl * per_s;
+    const std::int64_t z = tz / per_z;
+    tile_coords(tz - z * per_z, mo, no);
     double acc[3][9][2];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
       for (int j = 0; j < 9; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (std::int64_t ks = 0; ks < ksteps; ++ks, ++it) {
+    for (std::int64_t ks = k_lo(sl); ks < k_lo(sl + 1); ++ks, ++it) {
       const int s = static_cast<int>(it % S);
       const std::uint32_t round = static_cast<std::uint32_t>(it / S);
       ptx::mbar_wait(&full[s], round & 1u);
@@ -227,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // extent, filled with zeros by TMA) are not stored
     const std::int64_t gmo = mo * MT + mo_l, gno = no * NT + wn;
     if (gmo >= p.ext_mo || gno >= p.ext_no) continue;
-    double* cbase = p.C + z * p.c_z + gmo * p.c_mo + gno * p.c_no;
+    double* cbase = (p.ksplit > 1 ? p.ws + sl * p.csize : p.C) + z * p.c_z + gmo * p.c_mo + gno * p.c_no;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       const int m = m0 + i * 8 + qrow;
@@ -276,6 +286,16 @@ __global__ void rowsum_kernel(const double* __restrict__ X, double* __restrict__
   double t = (s[0] + s[1]) + (s[2] + s[3]);
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   if (lane == 0) rows[warp] = t;
+}
+
+// C[i] = sum over slices of ws[s * n + i], slices in order
+__global__ void ksplit_reduce_kernel(const double* __restrict__ ws, double* __restrict__ C, std::int64_t n, int ks) {
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    double v = ws[i];
+    for (int s = 1; s < ks; ++s) v += ws[s * n + i];
+    C[i] = v;
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -353,6 +373,7 @@ int launch_gett(const GettLaunch& L, void* stream) {
   d.ka_steps = (L.ext_ka + KA - 1) / KA;
   d.kb_steps = (L.ext_kb + KB - 1) / KB;
   d.vec_c = L.c_ni == 1 && L.c_mi % 2 == 0 && L.c_mo % 2 == 0 && L.c_no % 2 == 0 && L.c_z % 2 == 0 &&
+            (L.ksplit <= 1 || (L.ext_mo * L.ext_mi * L.ext_no * L.ext_ni * (L.nz > 1 ? L.nz : 1)) % 2 == 0) &&
             (reinterpret_cast<std::uintptr_t>(L.C) & 15) == 0;
   d.c_mo = L.c_mo;
   d.c_mi = L.c_mi;
@@ -380,6 +401,9 @@ int launch_gett(const GettLaunch& L, void* stream) {
   }
   d.nz = nz;
   d.c_z = L.c_z;
+  d.ksplit = L.ksplit > 1 && L.ws && !(L.a_alpha >= 0 || L.b_alpha >= 0) ? L.ksplit : 1;
+  d.ws = L.ws;
+  d.csize = L.ext_mo * L.ext_mi * L.ext_no * L.ext_ni * nz;
   d.stages = L.stages > 0 ? L.stages : 3;
   d.group = L.group > 0 ? L.group : 6;
   const size_t smem = 1024 + static_cast<size_t>(d.stages) * 2 * kTileBytes + 16 * d.stages;
@@ -392,8 +416,13 @@ int launch_gett(const GettLaunch& L, void* stream) {
   if (per_sm < 1) per_sm = 1;
   std::int64_t grid = static_cast<std::int64_t>(sms) * per_sm;
   if (L.grid > 0) grid = L.grid;
-  if (grid > d.mo * d.no * nz) grid = d.mo * d.no * nz;
+  if (grid > d.mo * d.no * nz * d.ksplit) grid = d.mo * d.no * nz * d.ksplit;
   gett_kernel<<<static_cast<int>(grid), kThreads, smem, static_cast<cudaStream_t>(stream)>>>(d, tmA, tmB);
+  if (d.ksplit > 1) {
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ksplit_reduce_kernel<<<sms * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(d.ws, L.C, d.csize, d.ksplit);
+  }
   return cudaGetLastError();
 }
 

@@ -216,6 +216,10 @@ struct GettLaunch {
   // batch: an index of A, B and C (nz values, strides a_z / b_z / c_z; no
   // affine operands); nz <= 1 = none
   std::int64_t nz, a_z, b_z, c_z;
+  // split K (small tile counts): ksplit slices into ws (ksplit x the dense
+  // C size, C's strides), summed into C by a second pass; 0 / 1 = off
+  int ksplit;
+  double* ws;
 };
 
 int launch_gett(const GettLaunch& p, void* stream);

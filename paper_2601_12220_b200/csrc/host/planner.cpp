@@ -2118,7 +2118,8 @@ std::string describe(const Plan& p) {
     case Family::tt: launches += static_cast<int>(p.tt.rows.size()); break;
     case Family::gett:
       for (const auto& r : p.gett.rows) {
-        launches += 1 + (p.gett.pack_a ? 1 : 0) + (p.gett.pack_b ? 1 : 0) + (p.gett.c_f32 ? 1 : 0);
+        launches += 1 + (p.gett.pack_a ? 1 : 0) + (p.gett.pack_b ? 1 : 0) + (p.gett.c_f32 ? 1 : 0) +
+                    (p.gett.ksplit > 1 ? 1 : 0);
         if (r.a_alpha >= 0 || r.b_alpha >= 0) launches += 2;
       }
       break;

@@ -1362,6 +1362,48 @@ void upload_tables(Plan& p, GenericLaunch& g, const BatchedEinsum& e, bool dry_r
 bool bind_path(Plan& p, const PlanOptions& opt, std::string* why) {
   const BatchedEinsum& e = p.skel;
   const int n = e.n();
+  if (e.b() > 1 && !p.complex_mode && !p.functional && p.tabs.empty()) {
+    // several rows and no family for the whole batch: each row planned on
+    // its own (a family, a path or the generic kernel), taken when at least
+    // one row gets something better than the generic kernel
+    PlanOptions so = opt;
+    so.force_transform.clear();
+    so.meta_override.clear();
+    std::vector<PathStep> steps;
+    bool better = false;
+    try {
+      for (int r = 0; r < e.b(); ++r) {
+        BatchedEinsum row;
+        row.i_in = e.i_in;
+        row.i_out = e.i_out;
+        row.args = {e.args[static_cast<size_t>(r)]};
+        PathStep ps;
+        ps.plan = make_plan(row, so);
+        better = better || ps.plan->family != Family::generic;
+        for (const auto& L : ps.plan->leaves) {
+          int src = -1;
+          for (size_t i = 0; i < p.leaves.size(); ++i)
+            if (p.leaves[i].meta.name == L.meta.name) src = static_cast<int>(i);
+          if (src < 0 || L.storage != p.leaves[static_cast<size_t>(src)].storage) throw error(errc::usage, "row leaf");
+          ps.src.push_back(src);
+        }
+        if (ps.plan->outputs[0].storage != p.outputs[static_cast<size_t>(r)].storage) throw error(errc::usage, "row output");
+        ps.out = -1;
+        ps.out_row = r;
+        steps.push_back(std::move(ps));
+      }
+    } catch (const std::exception& ex) {
+      *why = std::string("path: ") + ex.what();
+      return false;
+    }
+    if (!better) {
+      *why = "path: no row has a better plan than the generic kernel";
+      return false;
+    }
+    p.path = std::move(steps);
+    p.inter_bytes = 0;
+    return true;
+  }
   if (e.b() != 1 || n < 2 || n > 12 || p.complex_mode || p.functional || !p.tabs.empty()) {
     *why = "path: one row of 2..12 plain real operands";
     return false;
@@ -1865,7 +1907,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
     for (const PathStep& st : plan.path) {
       std::vector<const void*> in;
       for (int src : st.src) in.push_back(src >= 0 ? d_in[src] : inter(-src - 1));
-      void* out = st.out < 0 ? d_out[0] : inter(st.out);
+      void* out = st.out < 0 ? d_out[st.out_row] : inter(st.out);
       execute(*st.plan, in.data(), &out, stream);
     }
     return;

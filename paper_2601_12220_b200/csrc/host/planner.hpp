@@ -131,7 +131,8 @@ struct Plan;
 struct PathStep {
   std::unique_ptr<Plan> plan;
   std::vector<int> src;  // per step-plan input: caller leaf (>= 0) or intermediate -(1 + id)
-  int out = -1;          // intermediate id, or -1: the caller's output
+  int out = -1;          // intermediate id, or -1: the caller's output out_row
+  int out_row = 0;
 };
 
 struct Plan {

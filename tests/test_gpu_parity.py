@@ -69,7 +69,7 @@ def test_default_plans_random(fe, ref, torch_cuda):
     bar of the reference."""
     picked = set()
     for seed in range(60):
-        e = ref.generate_random(seed, b_max=1, n_max=4, max_indices=6, shape_pool=[2, 3, 5, 8])
+        e = ref.generate_random(seed, b_max=1 + seed % 2, n_max=4, max_indices=6, shape_pool=[2, 3, 5, 8])
         b = ref.random_bindings(e, seed + 23)
         want = ref.evaluate(e, b)
         got = fe.evaluate(e, b)
@@ -131,20 +131,24 @@ def test_contraction_path(fe, ref, torch_cuda):
          "args": [[m("A", [3, 40, 64]), m("B", [64, 64]), m("C", [3, 64, 30])]]},
         # two operands, one with a private index: reduced first, then GETT
         {"i_out": ["a", "d"], "i_in": [["a", "x", "c"], ["c", "d"]], "args": [[m("A", [48, 6, 64]), m("B", [64, 40])]]},
+        # two rows: each row planned on its own (here: a path each)
+        {"i_out": ["a", "d"], "i_in": [["a", "b"], ["b", "c"], ["c", "d"]],
+         "args": [[m("A", [48, 64]), m("B", [64, 72]), m("C", [72, 40])], [m("A", [48, 64]), m("D", [64, 72]), m("C", [72, 40])]]},
     ]
     for k, e in enumerate(cases):
         plan = fe.Plan(einsum=e)
         assert plan.info["transform"] == "path/v1", (k, plan.info)
         b = ref.random_bindings(e, 80 + k)
-        got = run_plan(torch_cuda, plan, b)[0]
-        want = ref.evaluate(e, b)[0].real
-        assert rel_err(got, want) <= FP64_TOL, k
+        got = run_plan(torch_cuda, plan, b)
+        want = [w.real for w in ref.evaluate(e, b)]
+        for g, w in zip(got, want):
+            assert rel_err(g, w) <= FP64_TOL, k
         # float32 arrays: fp32 intermediates, the fp32 bar
-        e32 = {**e, "args": [[{**a, "dtype": "float32"} for a in e["args"][0]]]}
+        e32 = {**e, "args": [[{**a, "dtype": "float32"} for a in row] for row in e["args"]]}
         plan = fe.Plan(einsum=e32)
         assert plan.info["transform"] == "path/v1", (k, plan.info)
-        got = run_plan(torch_cuda, plan, b)[0]
-        assert got.dtype == np.float32 and rel_err(got, want) <= 1e-5, k
+        for g, w in zip(run_plan(torch_cuda, plan, b), want):
+            assert g.dtype == np.float32 and rel_err(g, w) <= 1e-5, k
 
 
 def test_generic_complex_bit_exact(fe, ref, torch_cuda):

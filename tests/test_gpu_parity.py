@@ -438,6 +438,22 @@ def test_gett_folded_groups_tccg6(fe, ref, torch_cuda):
         assert np.array_equal(got, ref.evaluate(e, b)[0].real), k
 
 
+@pytest.mark.parametrize("ks", ["ks=1", "ks=3", "ks=8"])
+def test_gett_split_k(fe, ref, torch_cuda, ks):
+    """Split K (slices of the k steps into a workspace, ordered reduce):
+    forced slice counts on a matmul and a batched matmul, exact on dyadic
+    data like the unsplit kernel."""
+    m = lambda n, s: {"name": n, "shape": s, "dtype": "float64"}  # noqa: E731
+    for k, e in enumerate([
+        {"i_out": ["a", "c"], "i_in": [["a", "b"], ["b", "c"]], "args": [[m("A", [96, 512]), m("B", [512, 72])]]},
+        {"i_out": ["z", "a", "c"], "i_in": [["z", "a", "b"], ["z", "b", "c"]], "args": [[m("A", [2, 48, 256]), m("B", [2, 256, 64])]]},
+    ]):
+        plan = fe.Plan(einsum=e, options={"transform": "gett_dmma/v1", "meta": ks})
+        b = ref.random_bindings(e, 120 + k)
+        got = run_plan(torch_cuda, plan, b)[0]
+        assert np.array_equal(got, ref.evaluate(e, b)[0].real), (ks, k)
+
+
 def test_gett_batched(fe, ref, torch_cuda):
     """A batch index (in A, B and C: batched matmul) rides on a fifth TMA
     dimension and the tile scheduler; repacks run per batch value in one

@@ -696,7 +696,7 @@ def test_hex_sumfact_large_sampled(fe, torch_cuda):
         assert err <= FP64_TOL, q
 
 
-@pytest.mark.parametrize("name", ["C4-f64", "C2-small", "C3"])
+@pytest.mark.parametrize("name", ["C4-f64", "C2-small", "C3", "C1-f32-large", "hex-f32", "matmul-split", "path3"])
 def test_execute_host_pipelined(fe, torch_cuda, name):
     """fe_plan_execute_host on plans above the pipelining threshold runs the
     chunked H2D / kernels / D2H pipeline (sub-plans along the shard axis on
@@ -708,6 +708,18 @@ def test_execute_host_pipelined(fe, torch_cuda, name):
         plan = fe.Plan(einsum=C.tensor_train(n=4096))
     elif name == "C2-small":
         plan = fe.Plan(einsum=C.hex_poisson(E=40_000, b=3))
+    elif name == "C1-f32-large":
+        plan = fe.Plan(einsum=C.fem_grad(E=2_000_000, dtype="float32"))
+    elif name == "hex-f32":
+        plan = fe.Plan(einsum=C.hex_poisson(E=40_000, b=3, dtype="float32"))
+    elif name == "matmul-split":
+        mm = lambda n, s: {"name": n, "shape": s, "dtype": "float64"}  # noqa: E731
+        plan = fe.Plan(einsum={"i_out": ["a", "c"], "i_in": [["a", "b"], ["b", "c"]],
+                               "args": [[mm("A", [4096, 2048]), mm("B", [2048, 1024])]]})
+    elif name == "path3":
+        mm = lambda n, s: {"name": n, "shape": s, "dtype": "float64"}  # noqa: E731
+        plan = fe.Plan(einsum={"i_out": ["a", "d"], "i_in": [["a", "b"], ["b", "c"], ["c", "d"]],
+                               "args": [[mm("A", [4096, 512]), mm("B", [512, 512]), mm("C", [512, 1024])]]})
     else:
         plan = fe.Plan(kernel=C.tccg_kernel(ext=72))
     ins = []
@@ -725,7 +737,10 @@ def test_execute_host_pipelined(fe, torch_cuda, name):
         plan.execute_host([h.data_ptr() for h in hin], [h.data_ptr() for h in hout], s.cuda_stream)
         torch.cuda.synchronize()
         for g, w in zip(hout, want):
-            assert torch.equal(g, w.cpu()), name
+            if name == "path3":  # chunked sub-plans may split K differently: rounding of the 2nd step
+                assert rel_err(g.numpy(), w.cpu().numpy()) <= FP64_TOL, name
+            else:
+                assert torch.equal(g, w.cpu()), name
 
 
 @pytest.mark.parametrize("spec", [

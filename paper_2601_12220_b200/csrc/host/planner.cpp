@@ -769,6 +769,9 @@ bool bind_gett_split(Plan& p, std::string* why) {
       const bool y_inner = by_c ? y.c < x.c : (M == grp ? y.a < x.a : y.b < x.b);
       *in = y_inner ? y : x;
       *outer = y_inner ? x : y;
+      // the box dim (72 rows) should be as full as possible: take the other
+      // index when the stride-preferred one does not fit or fills under 2/3
+      if ((!(in->ext >= 24 && in->ext <= 72) || in->ext < 48) && outer->ext >= 48 && outer->ext <= 72) std::swap(*in, *outer);
       if (!(in->ext >= 24 && in->ext <= 72) && outer->ext >= 24 && outer->ext <= 72) std::swap(*in, *outer);
       return in->ext >= 24 && in->ext <= 72;
     }

@@ -4,7 +4,7 @@ Pinned spellings (the builder's choice, recorded in DESIGN.md):
 
 C1  FEM P2-tet gradient   xre,xij,ej->rei, b=3 fields, E=1e4, fp64
 C2  FEM P4-hex Poisson    xai,xbm,xcn,xyeabc,yaj,ybk,ycl,ejkl->eimn, b=8, E=2e6
-C3  TCCG abcd-aebf-dfce   aebf,dfce->abcd at extent 72, operands alpha*A+beta
+C3  TCCG abcd-aebf-dfce   aebf,dfce->abcd at extent 72, operands (a1*A+b1)(a2*B+b2)
 C4  tensor-train layer    ij,kl,njl->nik, n=4096, 64^4 per sample, fp64 / fp32
 C5  FEM wave step         C1 skeleton at E=2e6 with s_q = u_q + 0.5 k_q fused
 
@@ -67,21 +67,24 @@ def tccg(name="abcd-aebf-dfce", ext=72, dtype="float64"):
 
 
 def tccg_kernel(name="abcd-aebf-dfce", ext=72, a_ext=None):
-    """C3 with the TCCG protocol's functional operands alpha*A+beta
-    (PAPER.md:1708-1716), as a .fk kernel. ``a_ext`` overrides the extent of
-    output index a (the multi-GPU shard axis)."""
+    """C3 with the TCCG protocol's functional operands (alpha1*A+beta1) and
+    (alpha2*B+beta2), four separate runtime scalars, as a
+    .fk kernel. ``a_ext`` overrides the extent of output index a (the
+    multi-GPU shard axis)."""
     a, b = TCCG_SIBLINGS[name]
     lens = {s: ext for s in "abcdef"}
     lens["a"] = a_ext or ext
     da = "x".join(str(lens[s]) for s in a)
     db = "x".join(str(lens[s]) for s in b)
     return (f"domain: a<{lens['a']} b<{ext} c<{ext} d<{ext} e<{ext} f<{ext}\n"
-            "def opA(p,q,r,s) := alpha[]*A[p,q,r,s] + beta[]\n"
-            "def opB(p,q,r,s) := alpha[]*B[p,q,r,s] + beta[]\n"
+            "def opA(p,q,r,s) := alpha1[]*A[p,q,r,s] + beta1[]\n"
+            "def opB(p,q,r,s) := alpha2[]*B[p,q,r,s] + beta2[]\n"
             f"array: A float64 {da}\n"
             f"array: B float64 {db}\n"
-            "array: alpha float64 scalar\n"
-            "array: beta float64 scalar\n"
+            "array: alpha1 float64 scalar\n"
+            "array: alpha2 float64 scalar\n"
+            "array: beta1 float64 scalar\n"
+            "array: beta2 float64 scalar\n"
             f"stmt C[a,b,c,d] = sum([e,f], opA({','.join(a)})*opB({','.join(b)}))\n")
 
 

@@ -8,9 +8,10 @@
 //   GEMM2  Y^T[(n,k), i] = sum_j T^T[(n,k), j] G1[i, j]   A = T^T (shared, SW128)
 //
 // fp32 accuracy from the TF32 datapath (3xTF32): every operand is split into
-// hi = tf32 truncation (exact) and lo = x - hi (exact in fp32), and each GEMM
-// accumulates hi*hi + hi*lo + lo*hi in fp32 (the dropped lo*lo term is
-// ~2^-20 relative); tests/test_gpu_parity.py holds it to the fp32 bar.
+// hi = tf32(x) and lo = tf32(x - hi), both rounded to nearest (split_tf32),
+// and each GEMM accumulates hi*hi + hi*lo + lo*hi in fp32 (the dropped
+// remainders are ~2^-22 relative and unbiased); tests/test_benched_parity.py
+// holds it to the flat fp32 bar (1e-5 against double).
 //
 // Warp roles (one CTA per SM, persistent over sample pairs):
 //   warp 16 — walks the schedule as a whole warp (uniform control flow keeps
@@ -63,7 +64,6 @@ constexpr std::uint32_t kXhCol = 384, kXlCol = 448;
 constexpr std::uint32_t idesc(std::uint32_t n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
 }
-constexpr std::uint32_t kHiMask = 0xFFFFE000u;  // fp32 -> tf32 truncation
 
 struct TTTcDev {
   std::int64_t nb, npairs;
@@ -151,7 +151,22 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, std::u
       : "memory");
 }
 
-__device__ __forceinline__ float hi_of(float x) { return __uint_as_float(__float_as_uint(x) & kHiMask); }
+// 3xTF32 split with round-to-nearest on both parts: hi = rna_tf32(x), lo =
+// rna_tf32(x - hi) (x - hi is exact in fp32). The tensor core truncates the
+// low 13 mantissa bits of an fp32 operand; with a truncated split every
+// dropped remainder has the sign of x, and the bias grows linearly over the
+// 4096 products of a TT output (measured 1.5e-5 against double on the
+// reference's random_bindings data); rounded parts leave unbiased remainders
+// below 2^-22 |x| (the fp32 bar of SURVEY.md §8c, 1e-5, holds flat).
+__device__ __forceinline__ float tf32_rna(float x) {
+  std::uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void split_tf32(float x, float& h, float& l) {
+  h = tf32_rna(x);
+  l = tf32_rna(x - h);
+}
 
 // one 3xTF32 GEMM over K = 64 (8 k-steps of 8), B = [Bh ; Bl] stacked on N:
 //   D[:, 0:128]  = Ah * [Bh ; Bl]^T     (N = 128: the hi*hi and hi*lo terms side by side)
@@ -234,12 +249,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int idx = tid + k * kThreads;
       if (idx >= R * R) break;
       const int r = idx >> 6, c = idx & 63;
-      const float a = va[k], b = vb[k];
-      const float ah = hi_of(a), bh = hi_of(b);
+      float ah, al, bh, bl;
+      split_tf32(va[k], ah, al);
+      split_tf32(vb[k], bh, bl);
       *reinterpret_cast<float*>(g2 + sw_off(r, c, 2 * R)) = ah;
-      *reinterpret_cast<float*>(g2 + sw_off(R + r, c, 2 * R)) = a - ah;
+      *reinterpret_cast<float*>(g2 + sw_off(R + r, c, 2 * R)) = al;
       *reinterpret_cast<float*>(g1 + sw_off(r, c, 2 * R)) = bh;
-      *reinterpret_cast<float*>(g1 + sw_off(R + r, c, 2 * R)) = b - bh;
+      *reinterpret_cast<float*>(g1 + sw_off(R + r, c, 2 * R)) = bl;
     }
   }
   if (warp == kEpiWarps) {
@@ -342,9 +358,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float hv = hi_of(xv[e]);
+          float hv, lv;
+          split_tf32(xv[e], hv, lv);
           h[c4 * 4 + e] = __float_as_uint(hv);
-          l[c4 * 4 + e] = __float_as_uint(xv[e] - hv);
+          l[c4 * 4 + e] = __float_as_uint(lv);
         }
       }
       tmem_st16(tl_row + kXhCol, h);
@@ -396,11 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = row >> 6, j = row & 63;
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-          const float x = __uint_as_float(v[c]);
-          const float h = hi_of(x);
+          float h, l;
+          split_tf32(__uint_as_float(v[c]), h, l);
           const std::uint32_t o = sw_off(n * 64 + cg * 16 + c, j, kRows);
           *reinterpret_cast<float*>(a2h(b) + o) = h;
-          *reinterpret_cast<float*>(a2l(b) + o) = x - h;
+          *reinterpret_cast<float*>(a2l(b) + o) = l;
         }
       }
       if (tid == 0) TT_TRACE(t, 12)

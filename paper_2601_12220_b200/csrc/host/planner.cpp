@@ -2084,7 +2084,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
         L.x_sn = static_cast<std::int64_t>(b.NJ) * b.NL;
         L.y_sn = static_cast<std::int64_t>(b.NI) * b.NK;
         L.stages = meta_int(plan.meta, "stages", 2);
-        if (L.fp32 && meta_int(plan.meta, "tc", 1) != 0 && tt_tc_supported(L))
+        if (L.fp32 && meta_int(plan.meta, "tc", 0) != 0 && tt_tc_supported(L))
           cuda_check(launch_tt_tc(L, stream), "tt tcgen05 kernel");
         else
           cuda_check(launch_tt(L, stream), "tt kernel");
@@ -2147,7 +2147,7 @@ std::string describe(const Plan& p) {
   switch (p.family) {
     case Family::fem_grad: pipe = meta_int(p.meta, "mma", 0) ? "dmma" : "dfma"; break;
     case Family::gett: pipe = "dmma"; break;
-    case Family::tt: pipe = (p.tt.fp32 && meta_int(p.meta, "tc", 1)) ? "tcgen05_tf32x3" : "dmma"; break;
+    case Family::tt: pipe = (p.tt.fp32 && meta_int(p.meta, "tc", 0)) ? "tcgen05_tf32x3" : "dmma"; break;
     case Family::hex: pipe = "dfma"; break;
     case Family::path: pipe = "dmma"; break;
     case Family::generic: pipe = "fma"; break;

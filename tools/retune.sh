@@ -10,5 +10,5 @@ $B tune tools/es/C5.fk --db "$DB" --reps 10 --candidates "stages=3;ept=2;te=64,s
 $B tune tools/es/C2.es --db "$DB" --reps 3 --candidates ",ne=2,v=1"
 $B tune tools/es/C3.fk --db "$DB" --reps 5 --candidates "stages=2;group=6,stages=2;group=12,stages=3;group=6,stages=3;group=12"
 $B tune tools/es/C4-f64.es --db "$DB" --reps 10 --candidates ""
-$B tune tools/es/C4-f32.es --db "$DB" --reps 10 --candidates ",tc=0"
+$B tune tools/es/C4-f32.es --db "$DB" --reps 10 --candidates ",tc=1"
 $B tune tools/es/C1L-f32.es --db "$DB" --reps 10 --candidates "stages=4;ept=2;te=68,stages=4;ept=2,stages=3;ept=2,stages=3;ept=2;te=64,stages=4"

@@ -92,6 +92,54 @@ __global__ void dmma_peak_kernel(double* sink, int iters, double seed) {
   if (s == 12345.678) sink[0] = s;
 }
 
+// which = 2: even warps run the DMMA loop, odd warps the DFMA loop (8x the
+// iterations: equal flops per warp) — tells whether the FP64 tensor path and
+// the FP64 FMA pipe can run concurrently (combined rate ~2x one of them) or
+// share one datapath (combined rate = the single-pipe rate)
+__global__ void mixed_peak_kernel(double* sink, int iters, double seed) {
+  if ((threadIdx.x >> 5) & 1) {
+    double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+           a7 = a0 + 7;
+    const double m = 0.999999, c = 1e-7;
+    for (int i = 0; i < 8 * iters; ++i) {
+      a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+    if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 12345.678) sink[0] = a0;
+  } else {
+    double d[8][2];
+    for (int k = 0; k < 8; ++k) d[k][0] = d[k][1] = seed * k;
+    const double a = 1.0 + threadIdx.x * 1e-9, b = 0.5;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(d[k][0]), "+d"(d[k][1])
+                     : "d"(a), "d"(b));
+    }
+    double s = 0;
+    for (int k = 0; k < 8; ++k) s += d[k][0] + d[k][1];
+    if (s == 12345.678) sink[0] = s;
+  }
+}
+
+// DFMA throughput with few warps: 16 independent chains per thread (the
+// kernel's ILP), one CTA of `threads` per SM
+__global__ void dfma16_kernel(double* sink, int iters, double seed) {
+  double a[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[k] = seed + threadIdx.x + k;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[k] = fma(a[k], m, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s += a[k];
+  if (s == 12345.678) sink[0] = s;
+}
+
 }  // namespace
 
 int fp64_peak(int which, double* tflops) {
@@ -103,20 +151,39 @@ int fp64_peak(int which, double* tflops) {
   cudaEvent_t t0, t1;
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
+  if (which >= 100) {  // which = 100 + warps per SM: DFMA, 16 chains per thread, one CTA per SM
+    const int warps = which - 100, its = 2048;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(t0);
+      dfma16_kernel<<<sms, warps * 32>>>(sink, its, 0.5);
+      cudaEventRecord(t1);
+      cudaEventSynchronize(t1);
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    *tflops = 2.0 * 16 * its * static_cast<double>(sms) * warps * 32 / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    cudaFree(sink);
+    return cudaGetLastError();
+  }
   const int blocks = sms * 4, threads = 256, iters = 4096;
   for (int rep = 0; rep < 2; ++rep) {
     cudaEventRecord(t0);
     if (which == 0)
       dfma_peak_kernel<<<blocks, threads>>>(sink, iters, 0.5);
-    else
+    else if (which == 1)
       dmma_peak_kernel<<<blocks, threads>>>(sink, iters, 0.5);
+    else
+      mixed_peak_kernel<<<blocks, threads>>>(sink, iters, 0.5);
     cudaEventRecord(t1);
     cudaEventSynchronize(t1);
   }
   float ms = 0;
   cudaEventElapsedTime(&ms, t0, t1);
-  const double flops = which == 0 ? 2.0 * 8 * iters * static_cast<double>(blocks) * threads
-                                  : 512.0 * 8 * iters * static_cast<double>(blocks) * (threads / 32);
+  const double flops = which == 0   ? 2.0 * 8 * iters * static_cast<double>(blocks) * threads
+                       : which == 1 ? 512.0 * 8 * iters * static_cast<double>(blocks) * (threads / 32)
+                                    : 2 * 512.0 * 8 * iters * static_cast<double>(blocks) * (threads / 64);
   *tflops = flops / (ms * 1e-3) / 1e12;
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);

@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfeinsum_b200.so")
+# FE_LIB_PATH: an alternative in-tree build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("FE_LIB_PATH") or os.path.join(_HERE, "lib", "libfeinsum_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "feinsum_b200.h")
 
 KINDS = {1: "domain", 2: "usage", 3: "io", 4: "cuda", 5: "internal"}

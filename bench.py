@@ -13,8 +13,14 @@ the launching stream; per-config times are max-reduced over ranks. FLOPs are
 the algorithmic (optimal pairwise contraction path) counts, operand FLOPs of
 functional operands included.
 
-Multi-GPU: each config is sharded along its element/batch axis (weak scaling:
-every rank holds the full per-GPU problem size); no collective on the hot path.
+Multi-GPU: each config is sharded along its element/batch axis, no collective
+on the hot path. --scaling weak (default): the global problem is world x the
+config, every rank holds one config-sized shard; --scaling strong: the config
+itself is split N ways (BASELINE config 2: one 2M-element mesh over 1-8 GPUs).
+Shard outputs are verified bitwise against an unsharded one-GPU evaluation.
+
+Extra lines (not in the geomean, one GPU): the launch floor, C1 in a CUDA
+graph, C1 at E=2e6, the TCCG siblings of C3, the 3xTF32 C4-f32.
 """
 import argparse
 import json
@@ -51,26 +57,41 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=2.0, help="target seconds per CPU sample")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: world x the config, one config-sized shard per rank; strong: the config split N ways")
+    ap.add_argument("--no-extras", action="store_true", help="skip the extra (non-geomean) lines")
     return ap.parse_args()
 
 
 # ------------------------------------------------------------------ specs --
 
 def spec(name, scale=1.0):
-    """(kind, payload, extra) for a config; scale shrinks the sharded axis."""
+    """(kind, payload) for a config; scale multiplies the sharded axis (world
+    copies for weak scaling, a fraction for the CPU samples). FE_BENCH_SCALE
+    shrinks the base extent first (reduced sizes for the multi-rank tests on
+    one GPU), so world x the base is exactly world one-GPU shards."""
     from paper_2601_12220_b200 import configs as C
+    env = float(os.environ.get("FE_BENCH_SCALE", "1"))
+
+    def ext(full, even=False):
+        base = max(2 if even else 1, int(full * env))
+        if even:
+            base = base // 2 * 2
+        v = max(2 if even else 1, int(round(base * scale)))
+        return v // 2 * 2 if even else v
+
     if name == "C1":
-        return "einsum", C.fem_grad(E=max(2, int(10_000 * scale) // 2 * 2))
+        return "einsum", C.fem_grad(E=ext(10_000, even=True))
     if name == "C2":
-        return "einsum", C.hex_poisson(E=max(1, int(2_000_000 * scale)))
+        return "einsum", C.hex_poisson(E=ext(2_000_000))
     if name == "C3":
-        return "kernel", C.tccg_kernel(ext=72, a_ext=max(1, int(72 * scale)))
+        return "kernel", C.tccg_kernel(ext=72, a_ext=max(1, int(round(72 * scale))))
     if name == "C4-f64":
-        return "einsum", C.tensor_train(n=max(1, int(4096 * scale)))
+        return "einsum", C.tensor_train(n=ext(4096))
     if name == "C4-f32":
-        return "einsum", C.tensor_train(n=max(1, int(4096 * scale)), dtype="float32")
+        return "einsum", C.tensor_train(n=ext(4096), dtype="float32")
     if name == "C5":
-        return "kernel", C.wave_kernel(E=max(2, int(2_000_000 * scale) // 2 * 2))
+        return "kernel", C.wave_kernel(E=ext(2_000_000, even=True))
     raise ValueError(name)
 
 
@@ -138,16 +159,43 @@ class ClockSampler:
 
 # ------------------------------------------------------------ GPU arm -----
 
+def bithash(torch, t):
+    """Exact checksum of a tensor's bit patterns (int64 sums wrap mod 2^64,
+    so the reduction order does not matter): equal hashes <=> bitwise equal
+    up to astronomically unlikely collisions."""
+    x = t.contiguous().view(-1)
+    x = x.view(torch.int64) if x.element_size() == 8 else x.view(torch.int32).to(torch.int64)
+    w = torch.arange(x.numel(), device=x.device, dtype=torch.int64) % 8191 + 1
+    return [int(x.sum().item()), int((x * w).sum().item())]
+
+
+def shard_dim(full_shape, part_shape):
+    """The dimension a shard plan cut (None: replicated array)."""
+    for d, (a, b) in enumerate(zip(full_shape, part_shape)):
+        if a != b:
+            return d
+    return None
+
+
 class Workload:
-    def __init__(self, name, rank, world, torch, fe, seed):
+    def __init__(self, name, rank, world, torch, fe, seed, scaling="weak", extra=None):
         # weak scaling: the global problem is `world` copies of the config along
         # its shard axis; each rank plans the global einsum (same canonical
         # form family, same tuned transform) and runs its 1/world shard, which
-        # is exactly the single-GPU config.
-        kind, payload = spec(name, scale=world) if world > 1 else spec(name)
-        full = fe.Plan(einsum=payload) if kind == "einsum" else fe.Plan(kernel=payload)
-        self.full = full
+        # is exactly the single-GPU config. strong scaling: the global problem
+        # is the config itself (C2: one 2M-element mesh split N ways); every
+        # rank fills the same global inputs from one seed and keeps its slice.
         self.name = name
+        self.scaling = scaling
+        self.options = (extra or {}).get("options")
+        if extra is not None:
+            kind, payload = extra["kind"], extra["payload"]
+        else:
+            kind, payload = spec(name, scale=world) if (world > 1 and scaling == "weak") else spec(name)
+        self.kind, self.payload = kind, payload
+        opts = self.options or {}
+        full = fe.Plan(einsum=payload, options=opts) if kind == "einsum" else fe.Plan(kernel=payload, options=opts)
+        self.full = full
         if world > 1:
             self.plan, self.lo, self.hi, self.axis = full.shard(rank, world)
         else:
@@ -162,14 +210,32 @@ class Workload:
         self.bytes = info["bytes"]
         self.ref_flops = info["reference_flops"]
         dev = torch.device("cuda", torch.cuda.current_device())
-        self.ins = []
-        for k, m in enumerate(self.plan.inputs):
-            t = torch.empty(m["shape"], dtype=fe._torch_dtype(m["storage"]), device=dev)
-            fe.fill_dyadic(t, seed * 1000 + k)
-            self.ins.append(t)
         self.seed = seed
+        if world > 1 and scaling == "strong":
+            self.ins = [t for t in self.slice_inputs(torch, fe, self.global_inputs(torch, fe, dev))]
+        else:
+            self.ins = []
+            for k, m in enumerate(self.plan.inputs):
+                t = torch.empty(m["shape"], dtype=fe._torch_dtype(m["storage"]), device=dev)
+                fe.fill_dyadic(t, seed * 1000 + k)
+                self.ins.append(t)
         self.outs = self.plan.alloc_outputs(dev)
         self.launches = int(info.get("launches", 1))  # kernels per execute (plan describe)
+
+    def global_inputs(self, torch, fe, dev):
+        ins = []
+        for k, m in enumerate(self.full.inputs):
+            t = torch.empty(m["shape"], dtype=fe._torch_dtype(m["storage"]), device=dev)
+            fe.fill_dyadic(t, self.seed * 1000 + k)
+            ins.append(t)
+        return ins
+
+    def slice_inputs(self, torch, fe, gins):
+        out = []
+        for g, mf, mp in zip(gins, self.full.inputs, self.plan.inputs):
+            d = shard_dim(mf["shape"], mp["shape"])
+            out.append(g if d is None else g.narrow(d, self.lo, self.hi - self.lo).contiguous())
+        return out
 
     def run(self, stream):
         self.plan.execute([t.data_ptr() for t in self.ins], [t.data_ptr() for t in self.outs], stream)
@@ -200,7 +266,8 @@ def gpu_arm(args):
     loads, skipped = [], {}
     for i, n in enumerate(names):
         try:
-            w = Workload(n, rank, world, torch, fe, seed=(i + 1) * 100 + rank)
+            w = Workload(n, rank, world, torch, fe, seed=(i + 1) * 100 + (rank if args.scaling == "weak" else 0),
+                         scaling=args.scaling)
         except fe.FeinsumError as ex:
             skipped[n] = str(ex)
             continue
@@ -257,9 +324,13 @@ def gpu_arm(args):
             fp64[label] = v.value
 
     def pipe_peak(pipe):
-        """(TFLOP/s, source) of the arithmetic pipe a kernel issues to."""
+        """(TFLOP/s, source) of the arithmetic pipe a kernel issues to. FP64
+        kernels (DFMA or DMMA) are held to the faster of the two measured FP64
+        rates: the two share one datapath (tools/fp64_mixed_probe.py), and
+        DMMA reaches the full rate where DFMA tops out ~10% lower."""
         if pipe in ("dfma", "dmma"):
-            return fp64.get(pipe, 0.0), "measured on this GPU by fe_fp64_peak (FP64 %s)" % pipe.upper()
+            best = max(fp64.values()) if fp64 else 0.0
+            return best, "max(DFMA, DMMA) measured on this GPU by fe_fp64_peak"
         if pipe == "tcgen05_tf32x3":
             # dense TF32 = half the measured bf16 rate; 3xTF32 spends three MMAs per product
             return peaks["bf16_tflops"] / 2 / 3, "MEASURED_PEAKS.json bf16_tflops / 2 (TF32) / 3 (3xTF32 passes)"
@@ -275,7 +346,7 @@ def gpu_arm(args):
         # peak for the DMMA kernels, DFMA peak for the DFMA kernels)
         fp_peak = pipe_peak(w.pipe)[0] * 1e12
         roof_t = max(w.bytes / (peaks["hbm_gbs"] * 1e9), w.flops / fp_peak if fp_peak else 0.0)
-        per[w.name] = {"ms": t * 1e3, "gflops": gflops, "gbs": w.bytes * world / t / 1e9,
+        per[w.name] = {"ms": t * 1e3, "gflops": gflops, "gbs": w.full.info["bytes"] / t / 1e9,
                        "transform": w.transform, "source": w.source, "flops": w.flops, "bytes": w.bytes,
                        "roof_ms": roof_t * 1e3, "roof_frac": roof_t / t,
                        "pipe": w.pipe,
@@ -312,7 +383,11 @@ def gpu_arm(args):
         except (OSError, ValueError, KeyError):
             pass
 
-    verify = verify_shards(loads, torch, fe, rank, world, dist, cdev) if world > 1 else None
+    extras = None
+    if world == 1 and not args.no_extras:
+        extras = extras_pass(args, torch, fe, stream, flush, peaks, pipe_peak)
+
+    verify = verify_shards(loads, torch, fe, rank, world, dist, cdev, args.scaling) if world > 1 else None
 
     e2e = None
     if not args.no_e2e and loads:
@@ -326,17 +401,19 @@ def gpu_arm(args):
         line = {
             "metric": "geomean GFLOP/s (and fraction of roofline) over TCCG+FEM batched einsums, 1-8 B200",
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64 (C4-f32: f32)", "data": "synthetic dyadic values m/2^19-1 generated on device",
             "config": {"workload": "TCCG+FEM suite " + ",".join(w.name for w in loads),
                        "suite": {n: CONFIG_DOC[n] for n in names}, "per_config": per, "skipped": skipped,
                        "l2": "flushed before every config launch: 256 MiB write, then the same 256 MiB read back (L2 cold for the inputs and clean)",
-                       "parallelism": f"dp{world} (element/batch-axis shards, no collective)",
+                       "parallelism": f"dp{world} (element/batch-axis shards, no collective; {args.scaling} scaling)",
                        "wall_s_timed_region": wall},
             "roofline": roof, "fp64_peak_tflops": fp64, "clocks": clocks.summary(),
             "gpu_launches": args.steps * sum(w.launches for w in loads),
             "e2e": e2e, "cpu_baseline": cpu,
         }
+        if extras is not None:
+            line["extras"] = extras
         if verify is not None:
             line["verify"] = verify
         print(json.dumps(line))
@@ -344,34 +421,144 @@ def gpu_arm(args):
         dist.destroy_process_group()
 
 
-def verify_shards(loads, torch, fe, rank, world, dist, cdev):
-    """Verification gather (outside the timed region): every rank's shard was
-    filled from its own seeds; each rank sends per-output checksums (sum and
-    sum of squares, fp64) to all ranks, and rank 0 recomputes every other
-    rank's shard on its own GPU from the same seeds and compares."""
+def verify_shards(loads, torch, fe, rank, world, dist, cdev, scaling):
+    """Verification (outside the timed region): every rank hashes the bit
+    patterns of its shard outputs (bithash) and all-gathers the hashes; rank 0
+    recomputes every shard on ONE GPU WITHOUT sharding and compares bitwise:
+      strong scaling: rank 0 runs the unsharded global plan on the same global
+        inputs once and hashes each rank's slice of its outputs;
+      weak scaling (the global problem is world x the one-GPU config and does
+        not fit one GPU): rank 0 rebuilds rank r's inputs from its seeds and
+        runs the standalone one-GPU config plan (its own plan and fact, not the
+        shard plan) on them.
+    Sharding never changes per-element arithmetic, so any difference fails."""
     report = {}
-    for k, w in enumerate(loads):
-        mine = torch.tensor([float(o.double().sum()) for o in w.outs] + [float(o.double().pow(2).sum()) for o in w.outs],
-                            dtype=torch.float64, device=cdev)
+    for w in loads:
+        mine = torch.tensor(sum((bithash(torch, o) for o in w.outs), []), dtype=torch.int64, device=cdev)
         got = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(got, mine)
         ok = True
         if rank == 0:
-            seed_base = w.seed - rank
-            for r in range(1, world):
-                ins = []
-                for j, m in enumerate(w.plan.inputs):
-                    t = torch.empty(m["shape"], dtype=fe._torch_dtype(m["storage"]), device="cuda")
-                    fe.fill_dyadic(t, (seed_base + r) * 1000 + j)
-                    ins.append(t)
-                outs = w.plan(*ins)
-                ref = torch.tensor([float(o.double().sum()) for o in outs] + [float(o.double().pow(2).sum()) for o in outs],
-                                   dtype=torch.float64)
-                ok = ok and torch.allclose(ref, got[r].cpu(), rtol=1e-12, atol=1e-9)
-                del ins, outs
+            dev = torch.device("cuda", torch.cuda.current_device())
+            if scaling == "strong":
+                full_outs = w.full(*w.global_inputs(torch, fe, dev))
+                for r in range(world):
+                    sh, lo, hi, _ = w.full.shard(r, world)
+                    want = []
+                    for o, mf, mp in zip(full_outs, w.full.outputs, sh.outputs):
+                        d = shard_dim(mf["shape"], mp["shape"])
+                        want += bithash(torch, o if d is None else o.narrow(d, lo, hi - lo))
+                    ok = ok and want == got[r].cpu().tolist()
+                del full_outs
+            else:
+                kind, payload = spec(w.name)
+                solo = fe.Plan(einsum=payload) if kind == "einsum" else fe.Plan(kernel=payload)
+                seed0 = w.seed - rank
+                for r in range(world):
+                    ins = []
+                    for j, m in enumerate(solo.inputs):
+                        t = torch.empty(m["shape"], dtype=fe._torch_dtype(m["storage"]), device=dev)
+                        fe.fill_dyadic(t, (seed0 + r) * 1000 + j)
+                        ins.append(t)
+                    want = sum((bithash(torch, o) for o in solo(*ins)), [])
+                    ok = ok and want == got[r].cpu().tolist()
+                    del ins
+            torch.cuda.synchronize()
             report[w.name] = bool(ok)
     return {"ok": all(report.values()), "per_config": report,
-            "method": "all_gather of per-shard output checksums; rank 0 recomputes each shard from its seeds"}
+            "method": ("bitwise (exact bit-pattern hashes) against the unsharded one-GPU result: "
+                       + ("the global plan on the global inputs" if scaling == "strong"
+                          else "the standalone one-GPU config plan on each rank's inputs"))}
+
+
+EXTRA_DOC = {
+    "C1-graph": "C1 executed 20 times back to back inside one CUDA graph, per-execute time (launch cost "
+                "amortised; the 10 MB working set is L2-resident after the first execute, so no HBM roofline)",
+    "C1-L": "the C1 skeleton at E=2e6 (SURVEY.md 8d: C1 is below launch latency; its large case is HBM-bound)",
+    "C3-aebf-fdec": "TCCG sibling abcd-aebf-fdec at extent 72, (a1*A+b1)(a2*B+b2) operands",
+    "C3-eafb-fdec": "TCCG sibling abcd-eafb-fdec at extent 72, (a1*A+b1)(a2*B+b2) operands",
+    "C3-eafd-fbec": "TCCG sibling abcd-eafd-fbec at extent 72, (a1*A+b1)(a2*B+b2) operands",
+    "C4-f32-tf32": "C4-f32 on the tcgen05 3xTF32 kernel (precision class b200-tf32: ~1e-5 against double, above "
+                   "the flat fp32 bar on some data, so not the suite's C4-f32)",
+}
+
+
+def extra_specs():
+    from paper_2601_12220_b200 import configs as C
+    return {
+        "C1-L": {"kind": "einsum", "payload": C.fem_grad(E=2_000_000)},
+        "C3-aebf-fdec": {"kind": "kernel", "payload": C.tccg_kernel("abcd-aebf-fdec")},
+        "C3-eafb-fdec": {"kind": "kernel", "payload": C.tccg_kernel("abcd-eafb-fdec")},
+        "C3-eafd-fbec": {"kind": "kernel", "payload": C.tccg_kernel("abcd-eafd-fbec")},
+        "C4-f32-tf32": {"kind": "einsum", "payload": C.tensor_train(n=4096, dtype="float32"),
+                        "options": {"device": "b200-tf32"}},
+    }
+
+
+def extras_pass(args, torch, fe, stream, flush, peaks, pipe_peak):
+    """Lines reported beside the suite and NOT in its geomean (one GPU, same
+    methodology: L2 flushed before every timed launch, CUDA events on the
+    launching stream): the launch floor (an empty kernel), C1 inside a CUDA
+    graph, C1's large case, the TCCG siblings of C3 and the 3xTF32 C4-f32."""
+    sh = stream.cuda_stream
+    steps = max(3, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn, warm=2):
+        for _ in range(warm):
+            fn()
+        tot = 0.0
+        for _ in range(steps):
+            fe.flush_l2(flush)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1) * 1e-3
+        return tot / steps
+
+    out = {"doc": EXTRA_DOC}
+    out["launch_floor_us"] = timed(lambda: fe.lib().fe_launch_probe(sh)) * 1e6
+
+    def roofline(w, t):
+        fp_peak = pipe_peak(w.pipe)[0] * 1e12
+        hbm_t = w.bytes / (peaks["hbm_gbs"] * 1e9)
+        roof_t = max(hbm_t, w.flops / fp_peak if fp_peak else 0.0)
+        return {"ms": t * 1e3, "gflops": w.flops / t / 1e9, "gbs": w.bytes / t / 1e9, "transform": w.transform,
+                "source": w.source, "pipe": w.pipe, "roof_ms": roof_t * 1e3, "roof_frac": roof_t / t,
+                "bound": "hbm" if hbm_t >= roof_t else w.pipe}
+
+    # C1 in a CUDA graph: 20 executes per replay
+    try:
+        w = Workload("C1", 0, 1, torch, fe, seed=11)
+        reps = 20
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            w.run(cs.cuda_stream)  # warm (lazy module load, attributes) outside the capture
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=cs):
+                for _ in range(reps):
+                    w.run(torch.cuda.current_stream().cuda_stream)
+        stream.wait_stream(cs)
+        t = timed(g.replay) / reps
+        r = roofline(w, t)
+        r.update({"executes_per_graph": reps, "roof_ms": None, "roof_frac": None,
+                  "note": "L2-resident after the first execute: no HBM roofline"})
+        out["C1-graph"] = r
+        del g, w
+    except Exception as ex:  # noqa: BLE001 — reported, never fatal
+        out["C1-graph"] = {"error": str(ex)}
+    for name, sp in extra_specs().items():
+        try:
+            w = Workload(name, 0, 1, torch, fe, seed=31, extra=sp)
+            out[name] = roofline(w, timed(lambda: w.run(sh)))
+            del w
+        except Exception as ex:  # noqa: BLE001
+            out[name] = {"error": str(ex)}
+        torch.cuda.empty_cache()
+    return out
 
 
 def e2e_pass(args, loads, torch, fe, world, dist, cdev=None):
@@ -404,7 +591,7 @@ def e2e_pass(args, loads, torch, fe, world, dist, cdev=None):
             tt = torch.tensor([t], dtype=torch.float64, device=cdev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t = tt.item()
-        rates.append(w.flops * world / t / 1e9)
+        rates.append(w.global_flops / t / 1e9)
         bi = sum(x.numel() * x.element_size() for x in hin)
         bo = sum(x.numel() * x.element_size() for x in hout)
         h2d += bi
@@ -413,7 +600,7 @@ def e2e_pass(args, loads, torch, fe, world, dist, cdev=None):
         # PCIe floor: both directions overlapped (the host pipeline runs H2D,
         # kernels and D2H of different chunks on three streams)
         floor = max(bi / bw["h2d_gbs"], bo / bw["d2h_gbs"]) / 1e9
-        per[w.name] = {"ms": t * 1e3, "gflops": w.flops * world / t / 1e9, "h2d_bytes": bi, "d2h_bytes": bo,
+        per[w.name] = {"ms": t * 1e3, "gflops": w.global_flops / t / 1e9, "h2d_bytes": bi, "d2h_bytes": bo,
                        "pcie_floor_ms": floor * 1e3, "pcie_frac": floor / t}
         del hin, hout
     return {"value": math.exp(sum(math.log(r) for r in rates) / len(rates)), "unit": "GFLOP/s",

@@ -139,8 +139,12 @@ int fe_fill_dyadic(void* d_ptr, int storage, int64_t count, uint64_t seed, void*
 int fe_flush_l2(void* d_scratch, int64_t bytes, void* stream);
 int fe_sm_count(void);
 /* measured FP64 throughput of the current device, TFLOP/s: which = 0 DFMA,
- * 1 DMMA (the FP64 roofline denominator; MEASURED_PEAKS.json has none) */
+ * 1 DMMA (the FP64 roofline denominator; MEASURED_PEAKS.json has none),
+ * 2 half the warps each (shared datapath?), 100 + w: DFMA with w warps/SM */
 int fe_fp64_peak(int which, double* tflops);
+/* launch one empty kernel on `stream` (the launch-latency floor a timed
+ * single execute cannot go below) */
+int fe_launch_probe(void* stream);
 
 #ifdef __cplusplus
 }

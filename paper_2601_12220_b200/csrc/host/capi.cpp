@@ -726,6 +726,8 @@ int fe_flush_l2(void* d_scratch, int64_t bytes, void* stream) {
 
 int fe_fp64_peak(int which, double* tflops) { return cuda_status(feb200::fp64_peak(which, tflops)); }
 
+int fe_launch_probe(void* stream) { return cuda_status(feb200::launch_probe(stream)); }
+
 int fe_sm_count(void) {
   int n = 0;
   if (feb200::device_sm_count(&n) != 0) return -1;

@@ -282,5 +282,6 @@ int permute4_widen(const float* src, double* dst, const std::int64_t ext[4], con
 int narrow_f64_f32(const double* src, float* dst, std::int64_t n, void* stream);
 // which: 0 = DFMA (CUDA cores), 1 = DMMA m8n8k4 (FP64 tensor cores)
 int fp64_peak(int which, double* tflops);
+int launch_probe(void* stream);
 
 }  // namespace feb200

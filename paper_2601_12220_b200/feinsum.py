@@ -64,6 +64,7 @@ def lib():
         L.fe_plan_num_outputs.argtypes = [ctypes.c_void_p]
         L.fe_fill_dyadic.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p]
         L.fe_flush_l2.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.fe_launch_probe.argtypes = [ctypes.c_void_p]
         L.fe_brute_force_isomorphic.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64,
                                                 ctypes.POINTER(ctypes.c_void_p)]
         L.fe_generate_random.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]

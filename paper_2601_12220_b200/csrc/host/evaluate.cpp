@@ -8,6 +8,7 @@
 // these functions throw errc::io.
 #include <cuda_runtime.h>
 
+#include <deque>
 #include <functional>
 #include <memory>
 
@@ -45,6 +46,7 @@ bool complex_dtype(Dtype t) { return t == Dtype::complex64 || t == Dtype::comple
 // Device buffers of one call; freed on scope exit.
 struct DeviceScratch {
   std::vector<void*> bufs;
+  std::deque<std::vector<double>> staged;
   cudaStream_t stream = nullptr;
   ~DeviceScratch() {
     if (stream) cudaStreamSynchronize(stream);
@@ -66,10 +68,13 @@ void* upload(DeviceScratch& ds, const DenseArray& a, int storage) {
     check(cudaMemcpyAsync(d, a.data.data(), n * 16, cudaMemcpyHostToDevice, ds.stream), "upload");
     return d;
   }
-  std::vector<double> re(n);
+  // staged real parts live until the stream has consumed them (pageable
+  // async copies only guarantee staging, so keep the buffer alive)
+  ds.staged.emplace_back(n);
+  std::vector<double>& re = ds.staged.back();
   for (size_t i = 0; i < n; ++i) re[i] = a.data[i].real();
   void* d = ds.alloc(n * 8);
-  check(cudaMemcpy(d, re.data(), n * 8, cudaMemcpyHostToDevice), "upload");
+  check(cudaMemcpyAsync(d, re.data(), n * 8, cudaMemcpyHostToDevice, ds.stream), "upload");
   return d;
 }
 

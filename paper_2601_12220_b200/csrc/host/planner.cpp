@@ -769,9 +769,11 @@ bool bind_gett_split(Plan& p, std::string* why) {
       const bool y_inner = by_c ? y.c < x.c : (M == grp ? y.a < x.a : y.b < x.b);
       *in = y_inner ? y : x;
       *outer = y_inner ? x : y;
-      // the box dim (72 rows) should be as full as possible: take the other
-      // index when the stride-preferred one does not fit or fills under 2/3
-      if ((!(in->ext >= 24 && in->ext <= 72) || in->ext < 48) && outer->ext >= 48 && outer->ext <= 72) std::swap(*in, *outer);
+      // the M box dim (72 rows) should be as full as possible: take the other
+      // index when the stride-preferred one fills it under 2/3. N keeps C's
+      // unit-stride index (coalesced, vectorised epilogue stores) unless it
+      // does not fit at all.
+      if (!by_c && in->ext < 48 && outer->ext >= 48 && outer->ext <= 72) std::swap(*in, *outer);
       if (!(in->ext >= 24 && in->ext <= 72) && outer->ext >= 24 && outer->ext <= 72) std::swap(*in, *outer);
       return in->ext >= 24 && in->ext <= 72;
     }
@@ -1755,6 +1757,16 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
                             sizeof(double) * static_cast<size_t>(g.ext_mo * g.ext_mi * g.ext_no * g.ext_ni * g.nz)),
                  "cudaMalloc(gett f64 result)");
   }
+  // plan-time uploads (tables, literal coefficients) are pageable copies on
+  // the legacy stream; executes run on the caller's (possibly non-blocking)
+  // stream, so the DMA must be complete before the plan is handed out
+  if (!opt.dry_run && p.family == Family::hex) cuda_check(static_cast<cudaError_t>(hex_prepare(p.device)), "hex operator staging");
+  // executes that write plan-owned scratch are ordered across streams by an
+  // event (see execute), created here so the execute path never allocates
+  if (!opt.dry_run && (p.d_tab || p.d_inter || p.d_scratch || p.d_pack_a || p.d_pack_b || p.d_cbuf || p.d_ws ||
+                       (!p.chains.empty() && !p.coef_static)))
+    cuda_check(cudaEventCreateWithFlags(&p.last_use, cudaEventDisableTiming), "cudaEventCreate(plan scratch)");
+  if (!opt.dry_run) cuda_check(cudaStreamSynchronize(cudaStreamLegacy), "plan upload");
 }
 
 int leaf_storage_for(const ArrayMeta& m, const PlanOptions& opt) {
@@ -1774,6 +1786,7 @@ Plan::~Plan() {
   if (d_pack_b) cudaFree(d_pack_b);
   if (d_cbuf) cudaFree(d_cbuf);
   if (d_ws) cudaFree(d_ws);
+  if (last_use) cudaEventDestroy(last_use);
   if (d_tab) cudaFree(d_tab);
   if (d_inter) cudaFree(d_inter);
 }
@@ -1861,7 +1874,27 @@ std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,
   return p;
 }
 
+namespace {
+void execute_on(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream);
+std::mutex g_scratch_mu[16];
+}  // namespace
+
+// Plans that own mutable device scratch (tabulated operands, path
+// intermediates, GETT packs / K-sums / split-K workspace, per-execute
+// coefficients) serialise their executes: each waits for the previous one, on
+// whatever stream it ran, through the plan's last_use event. Plans without
+// scratch run concurrently on any number of streams.
 void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream) {
+  if (!plan.last_use) return execute_on(plan, d_in, d_out, stream);
+  std::lock_guard<std::mutex> lock(g_scratch_mu[(reinterpret_cast<std::uintptr_t>(&plan) >> 6) & 15]);
+  auto st = static_cast<cudaStream_t>(stream);
+  cuda_check(cudaStreamWaitEvent(st, plan.last_use, 0), "plan scratch ordering");
+  execute_on(plan, d_in, d_out, stream);
+  cuda_check(cudaEventRecord(plan.last_use, st), "plan scratch ordering");
+}
+
+namespace {
+void execute_on(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream) {
   const void* all_in[kMaxLeaves];
   const size_t nl = plan.leaves.size(), nt = plan.tabs.size();
   if (nt) {
@@ -2094,6 +2127,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
   }
   cuda_check(launch_generic(g, stream), "generic kernel");
 }
+}  // namespace
 
 void tabulate(const Plan& plan, const std::string& name, const void* const* d_in, double* d_out, std::int64_t first,
               std::int64_t count, void* stream) {

@@ -25,6 +25,7 @@
 #include "feinsum/raising.hpp"
 #include "../kernels/launch.h"
 
+struct CUevent_st;
 namespace feb200 {
 
 using feinsum::ArrayMeta;
@@ -197,6 +198,7 @@ struct Plan {
   double* d_pack_b = nullptr;
   double* d_cbuf = nullptr;     // GETT f64 result staging for fp32 outputs
   double* d_ws = nullptr;       // GETT split-K partial tiles
+  ::CUevent_st* last_use = nullptr;  // cudaEvent_t; orders executes that share the scratch above (null: no scratch)
   GenericLaunch gen{};  // pointers filled per execution
   int sm_count = 148;
 

@@ -21,273 +21,22 @@
 // path with FMA); parity is within 1e-12 relative.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
+#include "fem_grad.cuh"
 #include "launch.h"
-#include "ptx.cuh"
 
 namespace feb200 {
 
 namespace {
 
-struct Coef {
-  double pre, post;  // 1.0 when absent (x * 1.0 == x exactly)
-  int sign;
-};
-
-// element type: fp64 (C1 / C5) or fp32 (float32 einsums of the same shape;
-// the same kernel with half the bytes per element)
-template <typename T>
-struct Vec2;
-template <>
-struct Vec2<double> {
-  using type = double2;
-};
-template <>
-struct Vec2<float> {
-  using type = float2;
-};
-__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
-__device__ __forceinline__ double2 mk2(double a, double b) { return make_double2(a, b); }
-__device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, b); }
-
-// kDSmem: read D from shared memory (broadcast LDS.128) instead of holding
-// D[x,i,:] in 60 registers — halves the register footprint so two CTAs fit
-// per SM (more warps in flight for the HBM-bound loop); chosen per fact meta.
-// EPT: elements per consumer thread (el, el + TE/EPT, ...): more independent
-// FMA chains per thread and D reused from registers across them.
-// Consumer threads: TE * NI / EPT, padded to whole warps (tiles such as
-// TE = 34 / 68 that make E = 1e4 exactly one tile per CTA slot leave a few
-// padding threads idle).
-template <int NX, int NR, int NI, int NJ, int TE, int EPT>
-constexpr int fem_consumers() {
-  return (TE * NI / EPT + 31) / 32 * 32;
-}
+using namespace fem;
 
 template <typename T, int NX, int NR, int NI, int NJ, int TE, bool kPlainU, bool kDSmem, int EPT = 1>
 __global__ void __launch_bounds__(32 + fem_consumers<NX, NR, NI, NJ, TE, EPT>(), kDSmem ? 2 : 1)
     fem_grad_kernel(const __grid_constant__ FemGradLaunch p) {
-  using V2 = typename Vec2<T>::type;
-  static_assert(TE * sizeof(T) % 16 == 0, "bulk-copy rows are 16-byte multiples");
-  constexpr int kConsumers = fem_consumers<NX, NR, NI, NJ, TE, EPT>();
-  constexpr int kWorkers = TE * NI / EPT;  // consumers with an (element, i) task
-  constexpr int kES = TE / EPT;  // element stride between a thread's elements
-  static_assert(TE % EPT == 0 && TE % 2 == 0, "tile shape");
-  constexpr int kConsumerWarps = kConsumers / 32;
-  static_assert(NJ % 2 == 0, "U rows are read as double2");
-  constexpr int kUTile = TE * NJ;          // doubles per U tile
-  constexpr int kJTile = NX * NR * TE;     // doubles per J tile
-
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int S = p.stages;
-  const int stage_doubles = p.n_j * kJTile + p.n_u * kUTile;
-  T* dsm = reinterpret_cast<T*>(smem_raw);                         // D copies
-  T* ring = dsm + p.n_d * NX * NI * NJ;                            // stages
-  T* ucomb = ring + static_cast<size_t>(S) * stage_doubles;        // [2][rows][TE*NJ]
-  Coef* coefs = reinterpret_cast<Coef*>(
-      (reinterpret_cast<std::uintptr_t>(ucomb + (kPlainU ? 0 : 2 * p.rows * kUTile)) + 15) & ~std::uintptr_t{15});
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(coefs + kFemMaxUTiles);
-  std::uint64_t* empty = full + S;
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const std::int64_t E = p.E;
-  const std::int64_t ntiles = (E + TE - 1) / TE;
-
-  const std::uint64_t pol = ptx::policy_evict_first();
-  auto issue = [&](std::int64_t tile, int s) {
-    const std::int64_t e0 = tile * TE;
-    const int cnt = static_cast<int>(E - e0 < TE ? E - e0 : TE);
-    const std::uint32_t jb = static_cast<std::uint32_t>(cnt * sizeof(T));
-    const std::uint32_t ub = static_cast<std::uint32_t>(cnt * NJ * sizeof(T));
-    ptx::mbar_arrive_expect_tx(&full[s], static_cast<std::uint32_t>(p.n_j * NX * NR) * jb +
-                                             static_cast<std::uint32_t>(p.n_u) * ub);
-    T* st = ring + static_cast<size_t>(s) * stage_doubles;
-    for (int a = 0; a < p.n_j; ++a)
-      for (int xr = 0; xr < NX * NR; ++xr)
-        ptx::bulk_g2s_hint(st + a * kJTile + xr * TE, reinterpret_cast<const T*>(p.J[a]) + xr * E + e0, jb, &full[s], pol);
-    T* su = st + p.n_j * kJTile;
-    for (int u = 0; u < p.n_u; ++u)
-      ptx::bulk_g2s_hint(su + u * kUTile, reinterpret_cast<const T*>(p.U[u]) + e0 * NJ, ub, &full[s], pol);
-  };
-  // the producer thread starts the first S tile loads before the CTA-wide
-  // setup below, so their latency overlaps it (matters for small E, e.g. C1)
-  int prefetched = 0;
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], kConsumerWarps);
-    }
-    ptx::fence_barrier_init();
-    for (std::int64_t tile = blockIdx.x; tile < ntiles && prefetched < S; tile += gridDim.x, ++prefetched)
-      issue(tile, prefetched);
-  }
-  {
-    // D copies: every load of a thread issued before its stores (one global
-    // round trip in the prologue instead of one per loop trip)
-    constexpr int kPer = 4;
-    const int nd = p.n_d * NX * NI * NJ;
-    T v[kPer];
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int t = tid + k * static_cast<int>(blockDim.x);
-      const int which = t / (NX * NI * NJ);
-      v[k] = t < nd ? __ldg(reinterpret_cast<const T*>(p.D[which]) + (t - which * NX * NI * NJ)) : T(0);
-    }
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int t = tid + k * static_cast<int>(blockDim.x);
-      if (t < nd) dsm[t] = v[k];
-    }
-    for (int t = tid + kPer * static_cast<int>(blockDim.x); t < nd; t += blockDim.x) {
-      const int which = t / (NX * NI * NJ);
-      dsm[t] = __ldg(reinterpret_cast<const T*>(p.D[which]) + (t - which * NX * NI * NJ));
-    }
-  }
-  if (!kPlainU && tid < p.n_u) {
-    Coef c;
-    c.pre = p.u_pre[tid] >= 0 ? __ldg(p.coef + 2 * p.u_pre[tid]) : 1.0;
-    c.post = p.u_post[tid] >= 0 ? __ldg(p.coef + 2 * p.u_post[tid]) : 1.0;
-    c.sign = p.u_sign[tid];
-    coefs[tid] = c;
-  }
-  __syncthreads();
-
-  if (warp == 0) {
-    // ------------------------------ producer ------------------------------
-    if (tid != 0) return;
-    int it = 0;
-    for (std::int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      if (it < prefetched) continue;
-      const int s = it % S;
-      const std::uint32_t round = static_cast<std::uint32_t>(it / S);
-      ptx::mbar_wait(&empty[s], (round & 1u) ^ 1u);
-      issue(tile, s);
-    }
-    return;
-  }
-
-  // -------------------------------- consumers --------------------------------
-  const int c = tid - 32;
-  const int el = c / NI;
-  const int i = c - el * NI;
-  T dreg[kDSmem ? 1 : NX][kDSmem ? 2 : NJ];
-  int cur_d = -1;
-  int it = 0;
-  for (std::int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int s = it % S;
-    const std::uint32_t round = static_cast<std::uint32_t>(it / S);
-    ptx::mbar_wait(&full[s], round & 1u);
-    const std::int64_t e0 = tile * TE;
-    const T* st = ring + static_cast<size_t>(s) * stage_doubles;
-    const T* su = st + p.n_j * kJTile;
-
-    // K2 prologue: combine every row's U leaves once per tile
-    const T* ubase;
-    int urow_stride;
-    if (kPlainU) {
-      ubase = su;
-      urow_stride = kUTile;  // row q reads leaf tile row_u_first[q] == q
-    } else {
-      T* uc = ucomb + (it & 1) * p.rows * kUTile;
-      // (pre * leaf) * post per term, terms accumulated left to right — the
-      // operand's own order; two values per thread and iteration (16-byte
-      // shared accesses), the two-term form a*x +- b*y with its coefficients
-      // in registers
-      auto term = [](const Coef& cf, T v) { return mul_rn(mul_rn(static_cast<T>(cf.pre), v), static_cast<T>(cf.post)); };
-      auto join = [](const Coef& cf, T acc, T x) { return cf.sign > 0 ? add_rn(acc, x) : sub_rn(acc, x); };
-      for (int q = 0; q < p.rows; ++q) {
-        const int u0 = p.row_u_first[q], nt = p.row_u_count[q];
-        const V2* s0 = reinterpret_cast<const V2*>(su + u0 * kUTile);
-        V2* o = reinterpret_cast<V2*>(uc + q * kUTile);
-        if (nt == 2) {
-          const Coef c0 = coefs[u0], c1 = coefs[u0 + 1];
-          const V2* s1 = s0 + kUTile / 2;
-          for (int v = c; v < kUTile / 2; v += kConsumers) {
-            const V2 a = s0[v], b = s1[v];
-            o[v] = mk2(join(c1, term(c0, a.x), term(c1, b.x)), join(c1, term(c0, a.y), term(c1, b.y)));
-          }
-        } else {
-          for (int v = c; v < kUTile / 2; v += kConsumers) {
-            const Coef c0 = coefs[u0];
-            const V2 a = s0[v];
-            V2 acc = mk2(term(c0, a.x), term(c0, a.y));
-            for (int k = 1; k < nt; ++k) {
-              const Coef ck = coefs[u0 + k];
-              const V2 b = s0[k * (kUTile / 2) + v];
-              acc = mk2(join(ck, acc.x, term(ck, b.x)), join(ck, acc.y, term(ck, b.y)));
-            }
-            o[v] = acc;
-          }
-        }
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
-      ubase = uc;
-      urow_stride = kUTile;
-    }
-
-    if (c < kWorkers && e0 + el < E) {
-      for (int q = 0; q < p.rows; ++q) {
-        const T* dq_row = dsm + p.row_d[q] * NX * NI * NJ + i * NJ;  // D_q[x][i][:] at x*NI*NJ
-        if (!kDSmem && p.row_d[q] != cur_d) {
-          cur_d = p.row_d[q];
-          const T* dq = dsm + cur_d * NX * NI * NJ;
-#pragma unroll
-          for (int x = 0; x < NX; ++x)
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) dreg[x][j] = dq[(x * NI + i) * NJ + j];
-        }
-        (void)dq_row;
-        const T* ur = ubase + (kPlainU ? p.row_u_first[q] : q) * urow_stride + el * NJ;
-        T t[EPT][NX];
-#pragma unroll
-        for (int h = 0; h < EPT; ++h)
-#pragma unroll
-          for (int x = 0; x < NX; ++x) t[h][x] = T(0);
-#pragma unroll
-        for (int j = 0; j < NJ; j += 2) {
-          V2 u[EPT];
-#pragma unroll
-          for (int h = 0; h < EPT; ++h) u[h] = *reinterpret_cast<const V2*>(ur + h * kES * NJ + j);
-#pragma unroll
-          for (int x = 0; x < NX; ++x) {
-            T d0, d1;
-            if constexpr (kDSmem) {
-              const V2 dd = *reinterpret_cast<const V2*>(dq_row + x * NI * NJ + j);
-              d0 = dd.x;
-              d1 = dd.y;
-            } else {
-              d0 = dreg[x][j];
-              d1 = dreg[x][j + 1];
-            }
-#pragma unroll
-            for (int h = 0; h < EPT; ++h) {
-              t[h][x] = fma(d0, u[h].x, t[h][x]);
-              t[h][x] = fma(d1, u[h].y, t[h][x]);
-            }
-          }
-        }
-        const T* jt = st + p.row_j[q] * kJTile;
-        T* yq = reinterpret_cast<T*>(p.Y[q]);
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-#pragma unroll
-          for (int h = 0; h < EPT; ++h) {
-            T y = T(0);
-#pragma unroll
-            for (int x = 0; x < NX; ++x) y = fma(jt[(x * NR + r) * TE + el + h * kES], t[h][x], y);
-            if (h == 0 || e0 + el + h * kES < E)
-              __stcs(yq + (static_cast<std::int64_t>(r) * E + e0 + el + h * kES) * NI + i, y);
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if ((tid & 31) == 0) ptx::mbar_arrive(&empty[s]);
-  }
+  using Pro = typename std::conditional<kPlainU, FemProPlain, FemProAffine>::type;
+  fem_grad_body<T, NX, NR, NI, NJ, TE, Pro, kDSmem, EPT, FemEpiNone>(p);
 }
 
 template <typename T, int NX, int NR, int NI, int NJ, int TE, int EPT = 1>
@@ -349,6 +98,32 @@ int launch_fem_grad_t(const FemGradLaunch& p, cudaStream_t s) {
   if (p.NI == 4 && p.NJ == 4) return launch_shape<T, 3, 3, 4, 4, 64>(p, s);
   if (p.NI == 20 && p.NJ == 20) return launch_shape<T, 3, 3, 20, 20, 16>(p, s);
   return cudaErrorInvalidValue;
+}
+
+int launch_fem_grad_rtc(const FemGradLaunch& p, void* kernel, int te, int ept, void* stream) {
+  if (p.E == 0) return cudaSuccess;
+  const int nj = p.NJ, ni = p.NI;
+  const int threads = 32 + (te * ni / ept + 31) / 32 * 32;
+  const size_t doubles = static_cast<size_t>(p.n_d) * p.NX * ni * nj +
+                         static_cast<size_t>(p.stages) * (p.n_j * p.NX * p.NR * te + p.n_u * te * nj) +
+                         2 * static_cast<size_t>(p.rows) * te * nj;
+  const size_t smem = (p.f32 ? 4 : 8) * doubles + 16 + sizeof(Coef) * kFemMaxUTiles + sizeof(std::uint64_t) * 2 * p.stages;
+  const void* kern = kernel;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int sms = 148, per_sm = 1;
+  device_sm_count(&sms);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  const std::int64_t ntiles = (p.E + te - 1) / te;
+  std::int64_t grid = static_cast<std::int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+  if (p.grid > 0) grid = p.grid;
+  if (grid > ntiles) grid = ntiles;
+  void* args[] = {const_cast<FemGradLaunch*>(&p)};
+  return cudaLaunchKernel(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), args, smem,
+                          static_cast<cudaStream_t>(stream));
 }
 
 int launch_fem_grad(const FemGradLaunch& p, void* stream) {

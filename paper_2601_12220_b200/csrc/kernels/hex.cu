@@ -690,11 +690,10 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(g_hex_mu);
   HexConstSlot& slot = g_hex_slot[dev & 63];
-  if (slot.last) cudaStreamWaitEvent(st, slot.last, 0);
-  else if ((e = cudaEventCreateWithFlags(&slot.last, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if (!slot.last || !slot.stage) return cudaErrorInitializationError;  // hex_prepare() not run for this device
+  cudaStreamWaitEvent(st, slot.last, 0);
   // gather the six operators into one run, then one copy into the constant
   // bank (each copy costs tens of microseconds of stream time)
-  if (!slot.stage && (e = cudaMalloc(&slot.stage, 6 * ND * kMaxQ * kMaxQ * sizeof(double))) != cudaSuccess) return e;
   Mats6 m6{};
   for (int k = 0; k < 6; ++k) m6.m[k] = L.mats[k];
   gather_ops<T><<<1, 256, 0, st>>>(m6, ND * Q2, reinterpret_cast<T*>(slot.stage));
@@ -771,6 +770,17 @@ int launch_hex(const HexLaunch& L, void* stream) {
   if (grid > L.E / NE) grid = L.E / NE;
   hex_kernel<<<static_cast<int>(grid), kThreads, smem, static_cast<cudaStream_t>(stream)>>>(d);
   return cudaGetLastError();
+}
+
+// Creates the device's operator staging buffer and ordering event; called at
+// plan time so the execute path never allocates (and stays graph-capturable).
+int hex_prepare(int dev) {
+  std::lock_guard<std::mutex> lock(g_hex_mu);
+  HexConstSlot& slot = g_hex_slot[dev & 63];
+  cudaError_t e = cudaSuccess;
+  if (!slot.last && (e = cudaEventCreateWithFlags(&slot.last, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if (!slot.stage && (e = cudaMalloc(&slot.stage, 6 * ND * kMaxQ * kMaxQ * sizeof(double))) != cudaSuccess) return e;
+  return cudaSuccess;
 }
 
 }  // namespace feb200

@@ -4,7 +4,7 @@
 // kernel(s) on the given stream and returns a cudaError_t as int.
 #pragma once
 
-#include <cstdint>
+#include "rtc_std.h"
 
 namespace feb200 {
 
@@ -164,6 +164,7 @@ int launch_tabulate(const TabulateLaunch& p, void* stream);
 // tiles (plain operand = one term, no coefficients).
 constexpr int kFemMaxRows = 16;
 constexpr int kFemMaxUTiles = 32;
+constexpr int kFemMaxAux = 16;
 
 struct FemGradLaunch {
   int rows;
@@ -186,9 +187,15 @@ struct FemGradLaunch {
   bool f32;            // J, D, U, Y are float (pointers reinterpreted); E % 4 == 0
   const double* coef;  // interleaved complex coefficients (real part used)
   double* Y[kFemMaxRows];
+  // plan-time generated instances (codegen.cpp): arrays the fused operand
+  // programs / epilogues read outside the staged tiles
+  const void* aux[kFemMaxAux];
 };
 
 int launch_fem_grad(const FemGradLaunch& p, void* stream);
+// an NVRTC-compiled instance (codegen.cpp) of the same kernel body with tile
+// shape (te, ept): grid, block and shared memory sized like the prebuilt ones
+int launch_fem_grad_rtc(const FemGradLaunch& p, void* kernel, int te, int ept, void* stream);
 bool fem_grad_supported(int NX, int NR, int NI, int NJ);
 int launch_fem_mma(const FemGradLaunch& p, void* stream);
 bool fem_mma_supported(int NX, int NR, int NI, int NJ);
@@ -264,6 +271,7 @@ struct HexLaunch {
 };
 
 int launch_hex(const HexLaunch& p, void* stream);
+int hex_prepare(int device);  // plan time: operator staging + ordering event
 bool hex_supported(int nd, int p, std::int64_t E, int rows);
 
 // ---- utilities ----

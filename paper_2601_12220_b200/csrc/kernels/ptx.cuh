@@ -3,7 +3,7 @@
 // tensor-map TMA loads, and DMMA (mma.sync f64).
 #pragma once
 
-#include <cstdint>
+#include "rtc_std.h"
 
 namespace feb200 {
 namespace ptx {

@@ -413,7 +413,7 @@ int fe_plan_create_kernel(const char* fk, const char* options, fe_plan_t* out) {
     const RaiseResult rr = raise_to_batched_einsum(k);
     auto h = std::make_unique<fe_plan_s>();
     h->plan = feb200::make_functional_plan(rr.f.skeleton, rr.f.operand_map, k.arrays,
-                                           feb200::parse_options(options ? options : ""));
+                                           feb200::parse_options(options ? options : ""), rr.f.epilogue);
     h->options = options ? options : "";
     *out = h.release();
   });
@@ -431,8 +431,15 @@ int fe_plan_create_functional(const char* js, const char* options, fe_plan_t* ou
       ArrayMeta meta = transport::meta_from_json(m);
       arrays[meta.name] = meta;
     }
+    // extension: "epilogue": [{"row": r, "acc": name, "params": [...], "body": expr}, ...]
+    std::map<int, RowEpilogue> epi;
+    if (const Value* ev = v.find("epilogue"))
+      for (const auto& x : ev->a)
+        epi[static_cast<int>(x.at("row").as_int())] =
+            RowEpilogue{x.at("acc").as_str(),
+                        OperandExpr{transport::list_from_json(x.at("params")), expr_from(x.at("body"))}};
     auto h = std::make_unique<fe_plan_s>();
-    h->plan = feb200::make_functional_plan(skel, ops, arrays, feb200::parse_options(options ? options : ""));
+    h->plan = feb200::make_functional_plan(skel, ops, arrays, feb200::parse_options(options ? options : ""), epi);
     h->options = options ? options : "";
     *out = h.release();
   });

@@ -152,13 +152,17 @@ std::vector<DenseArray> evaluate_functional(const FunctionalBatchedEinsum& f, co
   for (const ArrayMeta& m : universe(f.skeleton))
     if (!f.operand_map.count(m.name)) throw error(errc::domain, "no operand expression for " + m.name);
   require_device();
-  const auto arrays = read_arrays(f.operand_map, bindings);
+  auto reads = f.operand_map;  // arrays read by operands and (extension) epilogues
+  for (const auto& [row, ep] : f.epilogue) reads["epilogue " + std::to_string(row)] = ep.op;
+  auto arrays = read_arrays(reads, bindings);
+  for (const auto& [row, ep] : f.epilogue) arrays.erase(ep.acc);
   std::vector<std::string> names;
   for (const auto& kv : arrays) names.push_back(kv.first);
   for (const auto& name : names)
     if (static_cast<std::int64_t>(bindings.at(name).data.size()) != bindings.at(name).meta.num_elements())
       throw error(errc::domain, "binding for array " + name + " has wrong element count");
-  auto plan = feb200::make_functional_plan(f.skeleton, f.operand_map, arrays, wide_options(bindings, names));
+  auto plan = feb200::make_functional_plan(f.skeleton, f.operand_map, arrays, wide_options(bindings, names),
+                                           f.epilogue);
   return run(*plan, bindings);
 }
 

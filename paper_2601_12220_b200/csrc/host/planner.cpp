@@ -199,7 +199,12 @@ struct OperandCompiler {
     for (size_t i = 0; i < p.leaves.size(); ++i) leaf_of[p.leaves[i].meta.name] = static_cast<int>(i);
   }
 
+  // epilogue compilation: reads of acc_name are the row's own value
+  std::string acc_name;
+  LeafInfo acc_info;
+
   const LeafInfo& leaf_checked(const std::string& name) {
+    if (!acc_name.empty() && name == acc_name) return acc_info;
     auto it = leaf_of.find(name);
     if (it == leaf_of.end()) throw error(errc::domain, "no binding for array " + name);
     return plan.leaves[it->second];
@@ -301,7 +306,7 @@ struct OperandCompiler {
           throw error(errc::domain, "array " + e.name + " read with " + std::to_string(e.subs.size()) +
                                         " subscripts, has " + std::to_string(L.meta.shape.size()) + " axes");
         VmRead rd{};
-        rd.leaf = leaf_of.at(e.name);
+        rd.leaf = (!acc_name.empty() && e.name == acc_name) ? kAccLeaf : leaf_of.at(e.name);
         rd.ndim = static_cast<int>(e.subs.size());
         if (rd.ndim > kMaxDims) throw error(errc::usage, "array " + e.name + " has too many axes for the device VM");
         std::int64_t stride = 1;
@@ -377,6 +382,46 @@ struct OperandCompiler {
     if (first)
       throw error(errc::domain, "array " + first->name + " subscript " + std::to_string(first->value) +
                                     " out of range on axis " + std::to_string(first->axis));
+  }
+
+  // RowEpilogue of a row with output shape out: always a VM program (run by
+  // generated code only); acc must be read pointwise (in-place safe)
+  OperandStatic compile_epilogue(const feinsum::RowEpilogue& ep, const ArrayMeta& out, int out_storage) {
+    if (ep.op.params.size() != out.shape.size())
+      throw error(errc::domain, "epilogue of " + ep.acc + " takes " + std::to_string(ep.op.params.size()) +
+                                    " parameters, the output has " + std::to_string(out.shape.size()) + " axes");
+    if (leaf_of.count(ep.acc)) throw error(errc::domain, "epilogue value " + ep.acc + " is also a bound array");
+    acc_name = ep.acc;
+    acc_info = LeafInfo{out, out_storage};
+    std::function<void(const Expr&)> check = [&](const Expr& e) {
+      for (const Expr& c : e.children) check(c);
+      if (e.kind != Expr::Kind::access) return;
+      if (e.name == ep.acc) {
+        if (e.subs != ep.op.params)
+          throw error(errc::domain, "epilogue reads " + ep.acc + " off its own point (only [" +
+                                        [&] {
+                                          std::string j;
+                                          for (const auto& x : ep.op.params) j += (j.empty() ? "" : ",") + x;
+                                          return j;
+                                        }() + "])");
+        return;
+      }
+      const LeafInfo& L = leaf_checked(e.name);
+      if (e.subs.size() != L.meta.shape.size())
+        throw error(errc::domain, "array " + e.name + " read with " + std::to_string(e.subs.size()) +
+                                      " subscripts, has " + std::to_string(L.meta.shape.size()) + " axes");
+    };
+    check(ep.op.body);
+    check_ranges(ep.op, out);
+    OperandStatic s{};
+    s.kind = OPK_VM;
+    s.ndim = static_cast<int>(out.shape.size());
+    s.prog_off = static_cast<int>(plan.prog.size());
+    emit(ep.op.body, 0, ep.op, out);
+    s.prog_len = static_cast<int>(plan.prog.size()) - s.prog_off;
+    if (uses_sqrt(ep.op.body)) throw error(errc::usage, "epilogues are real-valued (no sqrt)");
+    acc_name.clear();
+    return s;
   }
 
   OperandStatic compile(const OperandExpr& op, const ArrayMeta& sm) {
@@ -1666,8 +1711,9 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
   }
   p.transform = family_transform(p.family);
   if (!opt.meta_override.empty()) p.meta = opt.meta_override;
-  if (p.family == Family::generic && !p.tabs.empty()) {
-    // the generic kernel evaluates the programs in place: no tables
+  // tabulated operands back to their programs: the generic kernel (and the
+  // generated fem_grad instance) evaluate them in place, no tables
+  auto drop_tabs = [&] {
     const size_t bn = static_cast<size_t>(e.b()) * e.n(), nl = p.leaves.size();
     for (size_t i = 0; i < bn; ++i)
       if (p.ops[i].kind == OPK_PLAIN && static_cast<size_t>(p.ops[i].leaf) >= nl)
@@ -1675,6 +1721,65 @@ void finish_plan(Plan& p, const PlanOptions& opt) {
     p.ops.resize(bn);
     p.tabs.clear();
     p.tab_leaves.clear();
+  };
+  if (p.family == Family::generic && !p.tabs.empty()) drop_tabs();
+  // fem_grad with operand programs or epilogues: one generated instance of the
+  // kernel body (codegen.cpp) computes the programs in the prologue from the
+  // staged leaf tiles and applies the epilogues before the stores
+  if (p.family == Family::fem_grad && (!p.tabs.empty() || !p.epilogue.empty())) {
+    const FemBinding& f = p.fem;
+    int te = meta_int(p.meta, "te", f.NI == 10 ? 32 : (f.NI == 4 ? 64 : 16));
+    int ept = meta_int(p.meta, "ept", 1);
+    if (ept != 1 && ept != 2) ept = 1;
+    if (te < 2 || te > 128 || te % 2 != 0 || te % ept != 0) te = f.NI == 10 ? 32 : (f.NI == 4 ? 64 : 16);
+    const bool dsmem = ept == 1 && meta_int(p.meta, "dsmem", 0) != 0;
+    std::vector<std::vector<int>> tiles;
+    std::vector<int> aux;
+    std::string why, log;
+    if (!opt.codegen) {
+      p.fem_rtc_note = "prebuilt: codegen disabled";
+    } else {
+      const std::string src = fem_rtc_source(p, te, ept, dsmem, &tiles, &aux, &why);
+      void* kern = nullptr;
+      bool compiled = false;
+      if (!src.empty()) compiled = opt.dry_run ? nvrtc_compiles(src, &log)
+                                               : (kern = compile_rtc_kernel(src, "fe_fem_rtc", &log)) != nullptr;
+      if (src.empty()) {
+        p.fem_rtc_note = "prebuilt: " + why;
+      } else if (!compiled) {
+        p.fem_rtc_note = "prebuilt: " + log.substr(0, 300);
+      } else {
+        p.fem_rtc = kern;
+        p.fem_rtc_note = "nvrtc";
+        p.fem_rtc_te = te;
+        p.fem_rtc_ept = ept;
+        p.fem_rtc_tiles = tiles;
+        p.fem_rtc_aux = aux;
+        for (size_t q = 0; q < tiles.size(); ++q) {
+          p.fem.u_terms[q].clear();
+          for (int leaf : tiles[q]) p.fem.u_terms[q].push_back(AffineTerm{1, -1, leaf, -1, -1});
+        }
+        drop_tabs();
+      }
+    }
+  }
+  // epilogue passes (every family; the generated fem_grad instance fuses
+  // them, its runtime fallback to the generic kernel still needs them)
+  if (!p.epilogue.empty()) {
+    p.epi_pass.assign(static_cast<size_t>(e.b()), Plan::EpiPass{});
+    for (int r = 0; r < e.b(); ++r) {
+      if (p.epi_ops[static_cast<size_t>(r)].kind != OPK_VM) continue;
+      Plan::EpiPass& ep = p.epi_pass[static_cast<size_t>(r)];
+      const std::string src = epi_kernel_source(p, p.epi_ops[static_cast<size_t>(r)], p.outputs[static_cast<size_t>(r)].meta,
+                                                p.outputs[static_cast<size_t>(r)].storage, &ep.leaf_slots);
+      if (src.empty())
+        throw error(errc::usage, "epilogue of row " + std::to_string(r) + ": output storage " +
+                                     storage_name(p.outputs[static_cast<size_t>(r)].storage) +
+                                     " or more than 16 arrays read");
+      std::string log;
+      const bool ok = opt.dry_run ? nvrtc_compiles(src, &log) : (ep.kernel = compile_rtc_kernel(src, "fe_epi", &log)) != nullptr;
+      if (!ok) throw error(errc::io, "epilogue of row " + std::to_string(r) + " does not compile: " + log.substr(0, 300));
+    }
   }
 
   // generic launch (always prepared: it is also the runtime fallback)
@@ -1816,7 +1921,8 @@ std::unique_ptr<Plan> make_plan(const BatchedEinsum& e, const PlanOptions& opt) 
 
 std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,
                                            const std::map<std::string, OperandExpr>& operands,
-                                           const std::map<std::string, ArrayMeta>& arrays, const PlanOptions& opt) {
+                                           const std::map<std::string, ArrayMeta>& arrays, const PlanOptions& opt,
+                                           const std::map<int, feinsum::RowEpilogue>& epilogue) {
   feinsum::require_valid(skeleton);
   auto p = std::make_unique<Plan>();
   p->skel = skeleton;
@@ -1838,6 +1944,23 @@ std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,
   }
   for (int r = 0; r < skeleton.b(); ++r)
     for (int k = 0; k < skeleton.n(); ++k) p->ops.push_back(compiled.at(skeleton.args[r][k].name));
+  // row epilogues (extension): compiled against the row's output point
+  p->epilogue = epilogue;
+  if (!epilogue.empty()) {
+    if (p->complex_mode) throw error(errc::usage, "epilogues need a real-valued plan");
+    if (!opt.codegen) throw error(errc::usage, "epilogues run as generated code (option codegen: false given)");
+    OperandStatic none{};
+    none.kind = -1;
+    p->epi_ops.assign(static_cast<size_t>(skeleton.b()), none);
+    const auto lens = feinsum::index_lengths(skeleton);
+    for (const auto& [row, ep] : epilogue) {
+      if (row < 0 || row >= skeleton.b()) throw error(errc::domain, "epilogue for row " + std::to_string(row) + " of " +
+                                                                          std::to_string(skeleton.b()));
+      ArrayMeta out{ep.acc, {}, Dtype::float64};
+      for (const auto& ix : skeleton.i_out) out.shape.push_back(lens.at(ix));
+      p->epi_ops[static_cast<size_t>(row)] = cc.compile_epilogue(ep, out, ST_F64);
+    }
+  }
   // real-valued VM operands become tabulated leaves (Plan::tabs); finish_plan
   // drops them again if no tuned family binds
   constexpr std::int64_t kTabBudget = std::int64_t{1} << 30;  // doubles (8 GiB)
@@ -1875,8 +1998,22 @@ std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,
 }
 
 namespace {
-void execute_on(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream);
+void execute_on(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream, bool* epi_done);
 std::mutex g_scratch_mu[16];
+
+// the rows' epilogues as in-place passes over the outputs (families that do
+// not fuse them)
+void run_epilogues(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream) {
+  for (size_t r = 0; r < plan.epi_pass.size(); ++r) {
+    const Plan::EpiPass& ep = plan.epi_pass[r];
+    if (!ep.kernel) continue;
+    TabArgs args{};
+    for (size_t k = 0; k < ep.leaf_slots.size(); ++k) args.leaf[k] = d_in[ep.leaf_slots[k]];
+    args.out = static_cast<double*>(d_out[r]);
+    args.count = plan.outputs[r].meta.num_elements();
+    cuda_check(launch_tab_kernel(ep.kernel, args, plan.sm_count, stream), "generated epilogue kernel");
+  }
+}
 }  // namespace
 
 // Plans that own mutable device scratch (tabulated operands, path
@@ -1885,16 +2022,22 @@ std::mutex g_scratch_mu[16];
 // whatever stream it ran, through the plan's last_use event. Plans without
 // scratch run concurrently on any number of streams.
 void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream) {
-  if (!plan.last_use) return execute_on(plan, d_in, d_out, stream);
+  bool epi_done = false;
+  if (!plan.last_use) {
+    execute_on(plan, d_in, d_out, stream, &epi_done);
+    if (!epi_done) run_epilogues(plan, d_in, d_out, stream);
+    return;
+  }
   std::lock_guard<std::mutex> lock(g_scratch_mu[(reinterpret_cast<std::uintptr_t>(&plan) >> 6) & 15]);
   auto st = static_cast<cudaStream_t>(stream);
   cuda_check(cudaStreamWaitEvent(st, plan.last_use, 0), "plan scratch ordering");
-  execute_on(plan, d_in, d_out, stream);
+  execute_on(plan, d_in, d_out, stream, &epi_done);
+  if (!epi_done) run_epilogues(plan, d_in, d_out, stream);
   cuda_check(cudaEventRecord(plan.last_use, st), "plan scratch ordering");
 }
 
 namespace {
-void execute_on(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream) {
+void execute_on(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream, bool* epi_done) {
   const void* all_in[kMaxLeaves];
   const size_t nl = plan.leaves.size(), nt = plan.tabs.size();
   if (nt) {
@@ -1999,7 +2142,30 @@ void execute_on(const Plan& plan, const void* const* d_in, void* const* d_out, v
     L.ept = meta_int(plan.meta, "ept", 1);
     L.f32 = f.f32;
     L.mma = !f.f32 && meta_int(plan.meta, "mma", 0) != 0 && fem_mma_supported(L.NX, L.NR, L.NI, L.NJ);
-    if (ok) {
+    if (ok && plan.fem_rtc) {
+      // generated instance: staged tiles per row as generated, aux reads
+      int t = 0;
+      for (int q = 0; q < f.rows; ++q) {
+        L.row_u_first[q] = t;
+        L.row_u_count[q] = static_cast<int>(plan.fem_rtc_tiles[static_cast<size_t>(q)].size());
+        for (int leaf : plan.fem_rtc_tiles[static_cast<size_t>(q)]) {
+          L.U[t] = static_cast<const double*>(d_in[leaf]);
+          L.u_sign[t] = 1;
+          L.u_pre[t] = L.u_post[t] = -1;
+          ok = ok && aligned16(L.U[t]);
+          ++t;
+        }
+      }
+      L.n_u = t;
+      L.plain_u = false;
+      for (size_t k = 0; k < plan.fem_rtc_aux.size(); ++k) L.aux[k] = d_in[plan.fem_rtc_aux[k]];
+      if (ok) {
+        cuda_check(launch_fem_grad_rtc(L, plan.fem_rtc, plan.fem_rtc_te, plan.fem_rtc_ept, stream),
+                   "generated fem_grad kernel");
+        *epi_done = true;
+        return;
+      }
+    } else if (ok) {
       if (L.mma)
         cuda_check(launch_fem_mma(L, stream), "fem_mma kernel");
       else
@@ -2212,7 +2378,16 @@ std::string describe(const Plan& p) {
       break;
   }
   launches += static_cast<int>(p.tabs.size());
+  const bool epi_fused = p.fem_rtc_note == "nvrtc";
+  if (!epi_fused)
+    for (const auto& op : p.epi_ops) launches += op.kind == OPK_VM ? 1 : 0;
   v.set("launches", Value::num(launches));
+  // extension: row epilogues and the generated fem_grad instance
+  Value erows = Value::arr();
+  for (const auto& [row, ep] : p.epilogue) erows.push(Value::num(row));
+  v.set("epilogue_rows", std::move(erows));
+  v.set("epilogue_fused", Value::boolean_(epi_fused && !p.epilogue.empty()));
+  if (!p.fem_rtc_note.empty()) v.set("fem_codegen", Value::str(p.fem_rtc_note));
   Value tabs = Value::arr();
   Value gens = Value::arr();
   for (const auto& t : p.tabs) {
@@ -2376,6 +2551,17 @@ std::unique_ptr<Plan> make_shard(const Plan& full, int rank, int world, const Pl
       };
       walk(op.body);
     }
+    // epilogue reads: subscripts are output indices, sliced where they are the axis
+    for (const auto& [row, ep] : full.epilogue) {
+      std::function<void(const Expr&)> walk = [&](const Expr& x) {
+        for (const Expr& c : x.children) walk(c);
+        if (x.kind != Expr::Kind::access || x.name == ep.acc) return;
+        auto& flags = sliced[x.name];
+        flags.resize(x.subs.size(), false);
+        for (size_t d = 0; d < x.subs.size(); ++d) flags[d] = flags[d] || x.subs[d] == ix;
+      };
+      walk(ep.op.body);
+    }
     for (auto& [name, flags] : sliced) {
       auto& meta = arrays.at(name);
       for (size_t d = 0; d < flags.size(); ++d)
@@ -2384,7 +2570,7 @@ std::unique_ptr<Plan> make_shard(const Plan& full, int rank, int world, const Pl
           meta.shape[d] = b - a;
         }
     }
-    s = make_functional_plan(e, full.operand_exprs, arrays, o);
+    s = make_functional_plan(e, full.operand_exprs, arrays, o, full.epilogue);
   }
   s->meta = full.meta;
   s->source = "shard of " + full.source + " plan " + full.key;

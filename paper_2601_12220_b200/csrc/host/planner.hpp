@@ -198,12 +198,29 @@ struct Plan {
   double* d_pack_b = nullptr;
   double* d_cbuf = nullptr;     // GETT f64 result staging for fp32 outputs
   double* d_ws = nullptr;       // GETT split-K partial tiles
+  // ---- extension: row epilogues (RowEpilogue) and the generated fem_grad
+  // instance (codegen.cpp) that fuses operand programs and epilogues ----
+  std::map<int, feinsum::RowEpilogue> epilogue;  // caller row -> post-op, as given
+  std::vector<OperandStatic> epi_ops;  // per caller row: OPK_VM program (acc reads leaf kAccLeaf), or kind -1
+  struct EpiPass {
+    void* kernel = nullptr;            // NVRTC in-place pass over the row's output
+    std::vector<int> leaf_slots;
+  };
+  std::vector<EpiPass> epi_pass;       // per caller row (unfused families)
+  void* fem_rtc = nullptr;             // generated fem_grad instance (prologue programs + epilogues), or null
+  int fem_rtc_te = 0, fem_rtc_ept = 0;
+  std::vector<std::vector<int>> fem_rtc_tiles;  // per canonical row: staged U leaf tiles
+  std::vector<int> fem_rtc_aux;                 // FemGradLaunch::aux slot -> plan leaf
+  std::string fem_rtc_note;                     // describe(): "nvrtc" or why not
   ::CUevent_st* last_use = nullptr;  // cudaEvent_t; orders executes that share the scratch above (null: no scratch)
   GenericLaunch gen{};  // pointers filled per execution
   int sm_count = 148;
 
   ~Plan();
 };
+
+// VmRead::leaf of an epilogue's read of its own row value (RowEpilogue::acc).
+constexpr int kAccLeaf = -2;
 
 // Generated tabulation kernels (codegen.cpp).
 constexpr int kTabLeaves = 16;
@@ -214,7 +231,12 @@ struct TabArgs {
 };
 std::string tab_kernel_source(const Plan& p, const OperandStatic& op, const ArrayMeta& meta,
                               std::vector<int>* leaf_slots);
+std::string epi_kernel_source(const Plan& p, const OperandStatic& op, const ArrayMeta& out_meta, int out_storage,
+                              std::vector<int>* leaf_slots);
+std::string fem_rtc_source(const Plan& p, int te, int ept, bool dsmem, std::vector<std::vector<int>>* u_tiles,
+                           std::vector<int>* aux, std::string* why);
 void* compile_tab_kernel(const std::string& src, std::string* log);
+void* compile_rtc_kernel(const std::string& src, const char* name, std::string* log);
 bool nvrtc_compiles(const std::string& src, std::string* log);
 int launch_tab_kernel(void* kernel, const TabArgs& args, int sm_count, void* stream);
 
@@ -225,7 +247,8 @@ std::unique_ptr<Plan> make_plan(const BatchedEinsum& e, const PlanOptions& opt);
 std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,
                                            const std::map<std::string, OperandExpr>& operands,
                                            const std::map<std::string, ArrayMeta>& arrays,
-                                           const PlanOptions& opt);
+                                           const PlanOptions& opt,
+                                           const std::map<int, feinsum::RowEpilogue>& epilogue = {});
 
 // Enqueue the plan on `stream` with device pointers (inputs in plan->leaves
 // order, outputs in caller row order). Stream-ordered, allocation-free.

@@ -107,11 +107,13 @@ struct FemProAffine {  // affine combinations of leaf tiles (C5: u + 0.5 k)
   }
 };
 
-// ---- epilogue policies: pointwise map of each result value before its store ----
+// ---- epilogue policies: pointwise map of each result value before its store
+// (su: the stage's staged leaf tiles, which hold e0..e0+TE of every staged
+// [E, NJ] array, so epilogue reads of those come from shared memory) ----
 struct FemEpiNone {
   static constexpr bool kIdentity = true;
   template <typename T>
-  __device__ static T apply(const FemGradLaunch&, int, int, std::int64_t, int, T y) {
+  __device__ static T apply(const FemGradLaunch&, int, int, std::int64_t, int, T y, const T*, std::int64_t) {
     return y;
   }
 };
@@ -312,7 +314,7 @@ __device__ __forceinline__ void fem_grad_body(const FemGradLaunch& p) {
 #pragma unroll
             for (int x = 0; x < NX; ++x) y = fma(jt[(x * NR + r) * TE + el + h * kES], t[h][x], y);
             if (h == 0 || e0 + el + h * kES < E) {
-              if constexpr (!Epi::kIdentity) y = Epi::apply(p, q, r, e0 + el + h * kES, i, y);
+              if constexpr (!Epi::kIdentity) y = Epi::apply(p, q, r, e0 + el + h * kES, i, y, su, e0);
               __stcs(yq + (static_cast<std::int64_t>(r) * E + e0 + el + h * kES) * NI + i, y);
             }
           }

@@ -69,10 +69,19 @@ def test_vm_operands_planned_as_tables(fe):
     as a tabulated leaf feeding the tuned family; a complex one (sqrt) and a
     plan with no tuned family keep the in-place VM on the generic kernel."""
     from paper_2601_12220_b200 import configs as C
+    # fem_grad: the programs move into its generated prologue (no tables)
     p = fe.Plan(kernel=C.wave_kernel_nonlinear(E=2_000), options={"dry_run": True})
-    assert p.info["transform"] == "fem_grad/v1" and len(p.info["tabulated"]) == 3
+    assert p.info["transform"] == "fem_grad/v1" and p.info["tabulated"] == []
+    assert p.info["fem_codegen"] == "nvrtc"
     assert len(p.info["inputs"]) == 2 + 2 * 3  # caller inputs only
-    assert p.info["tab_codegen"] == ["nvrtc"] * 3  # the generated kernels compile for sm_100a
+    # tensor train: a transcendental core is tabulated by a generated kernel
+    fk = ("domain: n<64 i<64 j<64 k<64 l<64\n"
+          "def g(a,c) := exp(H[a,c] / 4)\n"
+          "array: H float64 64x64\narray: K float64 64x64\narray: X float64 64x64x64\n"
+          "stmt y[n,i,k] = sum([j,l], g(i,j)*K[k,l]*X[n,j,l])\n")
+    p = fe.Plan(kernel=fk, options={"dry_run": True})
+    assert p.info["transform"] == "tt/v1" and len(p.info["tabulated"]) == 1
+    assert p.info["tab_codegen"] == ["nvrtc"]  # the generated kernel compiles for sm_100a
     fk = ("domain: i<6 j<3\n"
           "def f(p) := sqrt(X[p]) * reciprocal(Y[p])\n"
           "array: X float64 6\narray: Y float64 6\narray: W float64 6x3\n"

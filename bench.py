@@ -480,6 +480,11 @@ EXTRA_DOC = {
     "C3-eafd-fbec": "TCCG sibling abcd-eafd-fbec at extent 72, (a1*A+b1)(a2*B+b2) operands",
     "C4-f32-tf32": "C4-f32 on the tcgen05 3xTF32 kernel (precision class b200-tf32: ~1e-5 against double, above "
                    "the flat fp32 bar on some data, so not the suite's C4-f32)",
+    "C5-nonlinear": "C5 skeleton with s = u*u - sin(k)/(2+exp(u)): the programs run in the prologue of a "
+                    "generated fem_grad instance (no operand tables in HBM); FP64-heavy (sin/exp/div per point)",
+    "C5-nonlinear-tables": "the same step with codegen off: device-VM tables in HBM + the prebuilt kernel",
+    "C5-post": "C5 (u + 0.5k) with a fused post epilogue per field, y <- u + 0.25 y (pre and post elementwise "
+               "fused: BASELINE config 5)",
 }
 
 
@@ -492,6 +497,10 @@ def extra_specs():
         "C3-eafd-fbec": {"kind": "kernel", "payload": C.tccg_kernel("abcd-eafd-fbec")},
         "C4-f32-tf32": {"kind": "einsum", "payload": C.tensor_train(n=4096, dtype="float32"),
                         "options": {"device": "b200-tf32"}},
+        "C5-nonlinear": {"kind": "kernel", "payload": C.wave_kernel_nonlinear()},
+        "C5-nonlinear-tables": {"kind": "kernel", "payload": C.wave_kernel_nonlinear(), "options": {"codegen": False}},
+        "C5-post": {"kind": "kernel", "payload": C.wave_kernel() + "".join(
+            f"epi y{q}[r,e,i] := u{q}[e,i] + 0.25*y{q}[r,e,i]\n" for q in (1, 2, 3))},
     }
 
 

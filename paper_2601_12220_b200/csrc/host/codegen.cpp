@@ -338,7 +338,7 @@ std::string fem_rtc_source(const Plan& p, int te, int ept, bool dsmem, std::vect
   std::ostringstream s;
   s << "#include \"fem_grad.cuh\"\n"
     << "using namespace feb200;\nusing namespace feb200::fem;\n"
-    << "struct GenPro {\n  static constexpr bool kPlain = false;\n"
+    << "struct GenPro {\n  static constexpr bool kPlain = false;\n  static constexpr bool kPipe = true;\n"
     << "  template <typename T, int kUTile, int kConsumers>\n"
     << "  __device__ static void combine(const FemGradLaunch& p, const T* su, T* uc, const Coef*, int c, long long e0,\n"
     << "                                 long long E) {\n"

@@ -2159,6 +2159,7 @@ void execute_on(const Plan& plan, const void* const* d_in, void* const* d_out, v
       L.n_u = t;
       L.plain_u = false;
       for (size_t k = 0; k < plan.fem_rtc_aux.size(); ++k) L.aux[k] = d_in[plan.fem_rtc_aux[k]];
+      if (L.stages < 2) L.stages = 2;  // the pipelined prologue reads one stage ahead
       if (ok) {
         cuda_check(launch_fem_grad_rtc(L, plan.fem_rtc, plan.fem_rtc_te, plan.fem_rtc_ept, stream),
                    "generated fem_grad kernel");

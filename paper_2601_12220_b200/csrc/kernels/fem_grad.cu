@@ -106,8 +106,9 @@ int launch_fem_grad_rtc(const FemGradLaunch& p, void* kernel, int te, int ept, v
   const int threads = 32 + (te * ni / ept + 31) / 32 * 32;
   const size_t doubles = static_cast<size_t>(p.n_d) * p.NX * ni * nj +
                          static_cast<size_t>(p.stages) * (p.n_j * p.NX * p.NR * te + p.n_u * te * nj) +
-                         2 * static_cast<size_t>(p.rows) * te * nj;
-  const size_t smem = (p.f32 ? 4 : 8) * doubles + 16 + sizeof(Coef) * kFemMaxUTiles + sizeof(std::uint64_t) * 2 * p.stages;
+                         3 * static_cast<size_t>(p.rows) * te * nj;  // pipelined prologue: 3 combined buffers
+  const size_t smem =
+      (p.f32 ? 4 : 8) * doubles + 16 + sizeof(Coef) * kFemMaxUTiles + sizeof(std::uint64_t) * (2 * p.stages + 3);
   const void* kern = kernel;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

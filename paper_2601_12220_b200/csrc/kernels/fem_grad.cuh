@@ -63,12 +63,14 @@ __device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, 
 // the stage's staged leaf tiles (su), once per tile ----
 struct FemProPlain {  // every row reads one leaf tile as is
   static constexpr bool kPlain = true;
+  static constexpr bool kPipe = false;
   template <typename T, int kUTile, int kConsumers>
   __device__ static void combine(const FemGradLaunch&, const T*, T*, const Coef*, int, std::int64_t, std::int64_t) {}
 };
 
 struct FemProAffine {  // affine combinations of leaf tiles (C5: u + 0.5 k)
   static constexpr bool kPlain = false;
+  static constexpr bool kPipe = false;
   template <typename T, int kUTile, int kConsumers>
   __device__ static void combine(const FemGradLaunch& p, const T* su, T* uc, const Coef* coefs, int c, std::int64_t,
                                  std::int64_t) {
@@ -150,11 +152,14 @@ __device__ __forceinline__ void fem_grad_body(const FemGradLaunch& p) {
   const int stage_doubles = p.n_j * kJTile + p.n_u * kUTile;
   T* dsm = reinterpret_cast<T*>(smem_raw);                         // D copies
   T* ring = dsm + p.n_d * NX * NI * NJ;                            // stages
-  T* ucomb = ring + static_cast<size_t>(S) * stage_doubles;        // [2][rows][TE*NJ]
+  // combined U tiles: 2 buffers, or 3 for the pipelined prologue (Pro::kPipe)
+  constexpr int kUBufs = kPlainU ? 0 : (Pro::kPipe ? 3 : 2);
+  T* ucomb = ring + static_cast<size_t>(S) * stage_doubles;        // [kUBufs][rows][TE*NJ]
   Coef* coefs = reinterpret_cast<Coef*>(
-      (reinterpret_cast<std::uintptr_t>(ucomb + (kPlainU ? 0 : 2 * p.rows * kUTile)) + 15) & ~std::uintptr_t{15});
+      (reinterpret_cast<std::uintptr_t>(ucomb + kUBufs * p.rows * kUTile) + 15) & ~std::uintptr_t{15});
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(coefs + kFemMaxUTiles);
   std::uint64_t* empty = full + S;
+  std::uint64_t* ufull = empty + S;  // kPipe: combined tile b complete (one arrive per consumer warp)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -185,6 +190,8 @@ __device__ __forceinline__ void fem_grad_body(const FemGradLaunch& p) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], kConsumerWarps);
     }
+    if constexpr (Pro::kPipe)
+      for (int b = 0; b < 3; ++b) ptx::mbar_init(&ufull[b], kConsumerWarps);
     ptx::fence_barrier_init();
     for (std::int64_t tile = blockIdx.x; tile < ntiles && prefetched < S; tile += gridDim.x, ++prefetched)
       issue(tile, prefetched);
@@ -240,11 +247,26 @@ __device__ __forceinline__ void fem_grad_body(const FemGradLaunch& p) {
   const int i = c - el * NI;
   T dreg[kDSmem ? 1 : NX][kDSmem ? 2 : NJ];
   int cur_d = -1;
+  // kPipe: the prologue of tile it+1 runs before the contraction of tile it,
+  // and readiness is an mbarrier per combined buffer instead of a CTA-wide
+  // named barrier, so warps drift up to one tile apart and one warp's
+  // (latency-bound) operand programs overlap another's contraction and
+  // stores. Three buffers: a warp writing tile it+1 can be one tile ahead
+  // of the slowest, which still reads tile it-1.
+  auto combine_tile = [&](int k, std::int64_t tl) {
+    const int sk = k % S;
+    ptx::mbar_wait(&full[sk], static_cast<std::uint32_t>(k / S) & 1u);
+    const T* sk_u = ring + static_cast<size_t>(sk) * stage_doubles + p.n_j * kJTile;
+    Pro::template combine<T, kUTile, kConsumers>(p, sk_u, ucomb + (k % 3) * p.rows * kUTile, coefs, c, tl * TE, E);
+    __syncwarp();
+    if ((tid & 31) == 0) ptx::mbar_arrive(&ufull[k % 3]);
+  };
+  if constexpr (Pro::kPipe)
+    if (blockIdx.x < ntiles) combine_tile(0, blockIdx.x);
   int it = 0;
   for (std::int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int s = it % S;
     const std::uint32_t round = static_cast<std::uint32_t>(it / S);
-    ptx::mbar_wait(&full[s], round & 1u);
     const std::int64_t e0 = tile * TE;
     const T* st = ring + static_cast<size_t>(s) * stage_doubles;
     const T* su = st + p.n_j * kJTile;
@@ -252,10 +274,18 @@ __device__ __forceinline__ void fem_grad_body(const FemGradLaunch& p) {
     // K2 prologue: combine every row's U leaves once per tile
     const T* ubase;
     int urow_stride;
-    if (kPlainU) {
+    if constexpr (Pro::kPipe) {
+      // (this thread waited on full[s] when it combined tile it)
+      if (tile + gridDim.x < ntiles) combine_tile(it + 1, tile + gridDim.x);
+      ptx::mbar_wait(&ufull[it % 3], static_cast<std::uint32_t>(it / 3) & 1u);
+      ubase = ucomb + (it % 3) * p.rows * kUTile;
+      urow_stride = kUTile;
+    } else if (kPlainU) {
+      ptx::mbar_wait(&full[s], round & 1u);
       ubase = su;
       urow_stride = kUTile;  // row q reads leaf tile row_u_first[q] == q
     } else {
+      ptx::mbar_wait(&full[s], round & 1u);
       T* uc = ucomb + (it & 1) * p.rows * kUTile;
       Pro::template combine<T, kUTile, kConsumers>(p, su, uc, coefs, c, e0, E);
       asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");

@@ -641,6 +641,173 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
   if (producer) ptx::bulk_wait<0>();
 }
 
+// ---------------------------------------------------------------- v5 -----
+// v2 with passes C and A of consecutive stages merged into one segment.
+//
+// The thread of pass C task (x, plane p, cube) reads W[x][cube][plane p] and
+// the thread of pass A task (y = x, plane j = p, cube) of the NEXT stage
+// writes exactly those 25 words — it is the same thread. So C(s) and A(s+1)
+// need no barrier between them: a stage costs two CTA barriers (after B;
+// after C+A) instead of three, and the tail of C (the direction-sum chain
+// into Ys, its named-barrier waits) overlaps the DFMAs of A. Direction 0
+// stores its partial before running A (nothing to wait for); directions 1 and
+// 2 run A first and then take their turn in the chain, so the chain's waits
+// are hidden behind A. Arithmetic and summation order are those of v2: the
+// output is bitwise identical.
+template <typename T, int Q, int X>
+__device__ __forceinline__ void sweep_c(const T* in, T (&v)[Q][Q]) {
+#pragma unroll
+  for (int b = 0; b < Q; ++b)
+#pragma unroll
+    for (int c = 0; c < Q; ++c) v[b][c] = in[b * Q + c];
+  cols_c<T, Q, 4, X, true>(v);
+  rows_c<T, Q, 5, X, true>(v);
+}
+
+template <typename T, int Q, int X>
+__device__ __forceinline__ void chain_store(const T (&v)[Q][Q], T* ys, int b0) {
+  if constexpr (X > 0) asm volatile("bar.sync %0, 64;" ::"r"(b0 + X - 1) : "memory");
+#pragma unroll
+  for (int m = 0; m < Q; ++m)
+#pragma unroll
+    for (int n = 0; n < Q; ++n) ys[m * Q + n] = X == 0 ? v[m][n] : ys[m * Q + n] + v[m][n];
+  if constexpr (X < 2) asm volatile("bar.arrive %0, 64;" ::"r"(b0 + X) : "memory");
+}
+
+// one thread's merged segment: C(s) on its W plane, A(s+1) into the same plane
+template <typename T, int Q, int D>
+__device__ __forceinline__ void c_then_a(T* w, T* ys, const T* a_in, int b0, bool next, std::uint64_t* ubar,
+                                         std::uint32_t uphase) {
+  T v[Q][Q];
+  sweep_c<T, Q, D>(w, v);
+  if constexpr (D == 0) chain_store<T, Q, 0>(v, ys, b0);
+  if (next) {
+    ptx::mbar_wait(ubar, uphase);
+    pass_a<T, Q, D>(a_in, w);
+  }
+  if constexpr (D > 0) chain_store<T, Q, D>(v, ys, b0);
+}
+
+template <typename T, int Q, int NE2, bool kSplitB>
+__global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex5_kernel(const __grid_constant__ Hex2Dev p) {
+  constexpr int NE = NE2;
+  constexpr int Q2 = Hx<Q>::Q2, Q3 = Hx<Q>::Q3, CS = Hx<Q>::CS;
+  static_assert(NE * kMaxFields == 32, "one warp per (direction, plane): 32 cubes per stage");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  const T* const pG = reinterpret_cast<const T*>(p.G);
+  constexpr int R = kMaxFields;
+  constexpr int nblk = NE * R;
+  constexpr int ds = nblk * CS;
+  T* Gs = sm;
+  T* Us = Gs + ND * ND * NE * Q3;
+  T* W = Us + R * NE * Q3;
+  T* Ys = W + ND * ds;
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(
+      (reinterpret_cast<std::uintptr_t>(Ys + R * NE * Q3) + 7) & ~std::uintptr_t{7});
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+
+  const std::int64_t nstages = p.E / NE;
+  const std::int64_t step = gridDim.x;
+  const std::uint32_t bytes = static_cast<std::uint32_t>(NE * Q3 * sizeof(T));
+  auto issue_g = [&](std::int64_t st) {
+    ptx::mbar_arrive_expect_tx(&bar[0], bytes * static_cast<std::uint32_t>(ND * ND));
+    const std::int64_t e0 = st * NE;
+    for (int xy = 0; xy < ND * ND; ++xy)
+      ptx::bulk_g2s(Gs + xy * NE * Q3, pG + (xy * p.E + e0) * Q3, bytes, &bar[0]);
+  };
+  auto issue_u = [&](std::int64_t st) {
+    ptx::mbar_arrive_expect_tx(&bar[1], bytes * static_cast<std::uint32_t>(R));
+    const std::int64_t e0 = st * NE;
+    for (int f = 0; f < R; ++f) ptx::bulk_g2s(Us + f * NE * Q3, reinterpret_cast<const T*>(p.U[f]) + e0 * Q3, bytes, &bar[1]);
+  };
+  const bool producer = threadIdx.x == blockDim.x - 32;
+  const std::int64_t st0 = blockIdx.x;
+  if (st0 >= nstages) return;
+  if (producer) {
+    issue_u(st0);
+    issue_g(st0);
+  }
+
+  // passes A and C: warp = (direction, plane), lane = cube
+  const int dir = threadIdx.x / (nblk * Q);
+  const int ptask = threadIdx.x - dir * nblk * Q;
+  const bool pactive = threadIdx.x < ND * nblk * Q;
+  const int pplane = ptask / nblk, pcube = ptask - pplane * nblk;
+  const T* a_in = Us + pcube * Q3 + pplane * Q2;
+  T* wp = W + dir * ds + pcube * CS + pplane * Q2;
+  T* ys = Ys + pcube * Q3 + pplane * Q2;
+  const int b0 = 1 + 2 * pplane;
+  constexpr int H = R / 2;
+  constexpr int nbt = H * NE * Q2;
+
+  // prologue: A of the first stage
+  if (pactive) {
+    ptx::mbar_wait(&bar[1], 0);
+    if (dir == 0) pass_a<T, Q, 0>(a_in, wp);
+    else if (dir == 1) pass_a<T, Q, 1>(a_in, wp);
+    else pass_a<T, Q, 2>(a_in, wp);
+  }
+  __syncthreads();
+  if (producer && st0 + step < nstages) issue_u(st0 + step);
+
+  int it = 0;
+  for (std::int64_t st = st0; st < nstages; st += step, ++it) {
+    const bool more = st + step < nstages;
+    ptx::mbar_wait(&bar[0], static_cast<std::uint32_t>(it & 1));
+    // pass B: the (line, element, field pair) tasks that fill whole
+    // four-warp rows run as pairs; the remainder is split into single-field
+    // tasks on one warp (at Q = 5: 384 pairs on warps 0-11, the last 16 pairs
+    // as 32 singles on warp 12), so no sub-partition issues a fourth
+    // full-length pass-B warp while the others issue three
+    constexpr int nfull = kSplitB ? nbt / 128 * 128 : nbt;
+    constexpr int nleft = nbt - nfull;
+    static_assert(2 * nleft <= 32, "remainder fits one warp");
+    if (threadIdx.x < nfull) {
+      const int t = threadIdx.x;
+      const int kl = t % Q2;
+      const int r = t / Q2;
+      const int el = r % NE, f0 = r / NE, f1 = f0 + H;
+      const T* g = Gs + el * Q3 + kl;
+      T* const wl[2] = {W + (f0 * NE + el) * CS + kl, W + (f1 * NE + el) * CS + kl};
+      pass_b<T, Q, 2>(wl, ds, g, NE * Q3);
+    } else if (nleft > 0 && threadIdx.x < nfull + 2 * nleft) {
+      const int idx = threadIdx.x - nfull;
+      const int t = nfull + (idx >> 1);
+      const int kl = t % Q2;
+      const int r = t / Q2;
+      const int el = r % NE, f = r / NE + ((idx & 1) ? H : 0);
+      const T* g = Gs + el * Q3 + kl;
+      T* const wl[1] = {W + (f * NE + el) * CS + kl};
+      pass_b<T, Q, 1>(wl, ds, g, NE * Q3);
+    }
+    if (producer) ptx::bulk_wait_read<0>();  // the previous stage's stores have read Ys
+    __syncthreads();
+    if (producer && more) issue_g(st + step);
+
+    if (pactive) {
+      const std::uint32_t uph = static_cast<std::uint32_t>((it + 1) & 1);
+      if (dir == 0) c_then_a<T, Q, 0>(wp, ys, a_in, b0, more, &bar[1], uph);
+      else if (dir == 1) c_then_a<T, Q, 1>(wp, ys, a_in, b0, more, &bar[1], uph);
+      else c_then_a<T, Q, 2>(wp, ys, a_in, b0, more, &bar[1], uph);
+    }
+    ptx::fence_proxy_async();
+    __syncthreads();  // Ys complete (stage st), Us consumed (stage st + step), W holds t of st + step
+    if (producer) {
+      const std::int64_t e0 = st * NE;
+      for (int f = 0; f < R; ++f) ptx::bulk_s2g(reinterpret_cast<T*>(p.Y[f]) + e0 * Q3, Ys + f * NE * Q3, bytes);
+      ptx::bulk_commit();
+      if (st + 2 * step < nstages) issue_u(st + 2 * step);
+    }
+  }
+  if (producer) ptx::bulk_wait<0>();
+}
+
 // The operator constants are shared by every launch on a device: a launch
 // waits for the previous one (any stream) before restaging them.
 struct HexConstSlot {
@@ -659,13 +826,15 @@ __global__ void gather_ops(const __grid_constant__ Mats6 src, int n, T* dst) {
 std::mutex g_hex_mu;
 HexConstSlot g_hex_slot[64];
 
-template <typename T, int Q, int NE2>
+template <typename T, int Q, int NE2, int kMerged = 0>
 int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
   constexpr int Q2 = Hx<Q>::Q2, Q3 = Hx<Q>::Q3, CS = Hx<Q>::CS;
   const int R = L.rows;
   const int nblk = NE2 * R;
   constexpr int threads = HexCfg<Q, NE2>::kThreads;
   auto kern = hex2_kernel<T, Q, NE2>;
+  if constexpr (kMerged == 1) kern = hex5_kernel<T, Q, NE2, false>;
+  if constexpr (kMerged == 2) kern = hex5_kernel<T, Q, NE2, true>;
   Hex2Dev d{};
   d.E = L.E;
   d.rows = R;
@@ -722,6 +891,12 @@ int launch_hex2_q(const HexLaunch& L, cudaStream_t st) {
     }
   }
   if constexpr (Q < 6) {
+    // v2 (default) takes the merged-stage kernel where it applies (eight
+    // fields: one warp per (direction, plane) over 32 cubes); v3 forces the
+    // three-barrier kernel, v5 the merged one without the pass-B split
+    const bool merged_ok = L.rows == kMaxFields && L.E % 4 == 0 && L.ne != 2;
+    if (merged_ok && L.variant == 5) return launch_hex2_t<double, Q, 4, 1>(L, st);
+    if (merged_ok && L.variant == 2) return launch_hex2_t<double, Q, 4, 2>(L, st);
     if (L.ne != 2 && L.E % 4 == 0) return launch_hex2_t<double, Q, 4>(L, st);
   }
   return launch_hex2_t<double, Q, 2>(L, st);

@@ -265,7 +265,9 @@ struct HexLaunch {
   const double* G;        // [ND, ND, E, P, P, P]
   const double* U[8];
   double* Y[8];
-  int variant;  // 2: constant-bank operators, plane/line passes (default); 1: register-plane passes
+  int variant;  // 2 (default): constant-bank operators, plane/line passes, C/A of consecutive stages merged
+                //   when rows == 8; 3: the three-barrier v2 kernel; 5: merged without the pass-B split;
+                //   1: register-plane passes
   int ne;       // v2 elements per stage: 4 (default when E % 4 == 0) or 2
   bool f32;     // every array float (pointers reinterpreted; v2 only, E % 4 == 0 below Q = 6)
 };

@@ -635,13 +635,17 @@ def test_tensor_train_f32_tensor_cores(fe, torch_cuda, n, meta):
 _HEX_WANT = {}
 
 
-@pytest.mark.parametrize("meta", ["", "ne=2", "v=1"])
+@pytest.mark.parametrize("meta", ["", "ne=2", "v=1", "v=3", "v=5"])
 def test_hex_sumfact_small(fe, ref, torch_cuda, meta):
-    """C2's sum-factorised operator at oracle-sized extents, both kernel
-    variants, with shared (A_d) and six distinct forward/backward operators."""
+    """C2's sum-factorised operator at oracle-sized extents, every kernel
+    variant (default: merged C/A stages with eight fields; v=3 the
+    three-barrier kernel; v=5 merged without the pass-B split; v=1 register
+    planes), with shared (A_d) and six distinct forward/backward operators."""
     from paper_2601_12220_b200 import configs as C
-    # E % 4 == 0 cases run the four-element stage, the others the two-element one
-    for E, b, distinct in [(2, 1, False), (4, 3, False), (2, 8, True), (6, 5, True), (4, 2, True), (8, 1, False)]:
+    # E % 4 == 0 cases run the four-element stage, the others the two-element
+    # one; b = 8 with E % 4 == 0 takes the merged-stage kernel
+    for E, b, distinct in [(2, 1, False), (4, 3, False), (2, 8, True), (6, 5, True), (4, 2, True), (8, 1, False),
+                           (8, 8, True), (12, 8, False)]:
         e = C.hex_poisson(E=E, b=b, distinct=distinct)
         opts = {"meta": meta, "transform": "hex_sumfact/v1"} if meta else None
         plan = fe.Plan(einsum=e, options=opts) if opts else fe.Plan(einsum=e)
@@ -810,7 +814,7 @@ def test_hex_other_orders(fe, torch_cuda, Q):
     counts (the two-element stage), against an fp64 torch.einsum."""
     from paper_2601_12220_b200 import configs as C
     torch = torch_cuda
-    for E, b, distinct in [(8, 3, True), (6, 8, False), (40, 5, True)]:
+    for E, b, distinct in [(8, 3, True), (6, 8, False), (40, 5, True), (8, 8, True)]:
         e = C.hex_poisson(E=E, b=b, P=Q, distinct=distinct)
         plan = fe.Plan(einsum=e)
         assert plan.info["transform"] == "hex_sumfact/v1", plan.info

@@ -654,6 +654,20 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
 // 2 run A first and then take their turn in the chain, so the chain's waits
 // are hidden behind A. Arithmetic and summation order are those of v2: the
 // output is bitwise identical.
+// FE_HEX_TRACE instance (meta v=7): per-warp clock64 stamps of CTA 0 for the
+// first kTraceIters stages, read back by tools/hex_trace.py through
+// fe_debug_hex_trace (not part of the ABI). ptxas may move a clock read
+// across independent arithmetic: only stamps next to waits are exact.
+constexpr int kTraceIters = 48, kTraceEv = 8;
+__device__ unsigned long long g_hex_trace[kTraceIters * 16 * kTraceEv];
+template <bool kTrace>
+__device__ __forceinline__ void hex_stamp(int it, int ev) {
+  if constexpr (kTrace) {
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && it < kTraceIters && threadIdx.x < 512)
+      g_hex_trace[(it * 16 + threadIdx.x / 32) * kTraceEv + ev] = clock64();
+  }
+}
+
 template <typename T, int Q, int X>
 __device__ __forceinline__ void sweep_c(const T* in, T (&v)[Q][Q]) {
 #pragma unroll
@@ -675,20 +689,23 @@ __device__ __forceinline__ void chain_store(const T (&v)[Q][Q], T* ys, int b0) {
 }
 
 // one thread's merged segment: C(s) on its W plane, A(s+1) into the same plane
-template <typename T, int Q, int D>
+template <typename T, int Q, int D, bool kTrace>
 __device__ __forceinline__ void c_then_a(T* w, T* ys, const T* a_in, int b0, bool next, std::uint64_t* ubar,
-                                         std::uint32_t uphase) {
+                                         std::uint32_t uphase, int it) {
   T v[Q][Q];
   sweep_c<T, Q, D>(w, v);
+  hex_stamp<kTrace>(it, 4);
   if constexpr (D == 0) chain_store<T, Q, 0>(v, ys, b0);
   if (next) {
     ptx::mbar_wait(ubar, uphase);
+    hex_stamp<kTrace>(it, 5);
     pass_a<T, Q, D>(a_in, w);
   }
+  hex_stamp<kTrace>(it, 6);
   if constexpr (D > 0) chain_store<T, Q, D>(v, ys, b0);
 }
 
-template <typename T, int Q, int NE2, bool kSplitB>
+template <typename T, int Q, int NE2, bool kSplitB, bool kTrace = false>
 __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex5_kernel(const __grid_constant__ Hex2Dev p) {
   constexpr int NE = NE2;
   constexpr int Q2 = Hx<Q>::Q2, Q3 = Hx<Q>::Q3, CS = Hx<Q>::CS;
@@ -759,7 +776,9 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex5_kernel(const
   int it = 0;
   for (std::int64_t st = st0; st < nstages; st += step, ++it) {
     const bool more = st + step < nstages;
+    hex_stamp<kTrace>(it, 0);
     ptx::mbar_wait(&bar[0], static_cast<std::uint32_t>(it & 1));
+    hex_stamp<kTrace>(it, 1);
     // pass B: the (line, element, field pair) tasks that fill whole
     // four-warp rows run as pairs; the remainder is split into single-field
     // tasks on one warp (at Q = 5: 384 pairs on warps 0-11, the last 16 pairs
@@ -777,26 +796,31 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex5_kernel(const
       T* const wl[2] = {W + (f0 * NE + el) * CS + kl, W + (f1 * NE + el) * CS + kl};
       pass_b<T, Q, 2>(wl, ds, g, NE * Q3);
     } else if (nleft > 0 && threadIdx.x < nfull + 2 * nleft) {
+      // lanes 0-15 take the first field of the remainder pairs, 16-31 the
+      // second: each half-warp walks consecutive lines (no bank conflicts)
       const int idx = threadIdx.x - nfull;
-      const int t = nfull + (idx >> 1);
+      const int t = nfull + idx % nleft;
       const int kl = t % Q2;
       const int r = t / Q2;
-      const int el = r % NE, f = r / NE + ((idx & 1) ? H : 0);
+      const int el = r % NE, f = r / NE + (idx >= nleft ? H : 0);
       const T* g = Gs + el * Q3 + kl;
       T* const wl[1] = {W + (f * NE + el) * CS + kl};
       pass_b<T, Q, 1>(wl, ds, g, NE * Q3);
     }
+    hex_stamp<kTrace>(it, 2);
     if (producer) ptx::bulk_wait_read<0>();  // the previous stage's stores have read Ys
     __syncthreads();
+    hex_stamp<kTrace>(it, 3);
     if (producer && more) issue_g(st + step);
 
     if (pactive) {
       const std::uint32_t uph = static_cast<std::uint32_t>((it + 1) & 1);
-      if (dir == 0) c_then_a<T, Q, 0>(wp, ys, a_in, b0, more, &bar[1], uph);
-      else if (dir == 1) c_then_a<T, Q, 1>(wp, ys, a_in, b0, more, &bar[1], uph);
-      else c_then_a<T, Q, 2>(wp, ys, a_in, b0, more, &bar[1], uph);
+      if (dir == 0) c_then_a<T, Q, 0, kTrace>(wp, ys, a_in, b0, more, &bar[1], uph, it);
+      else if (dir == 1) c_then_a<T, Q, 1, kTrace>(wp, ys, a_in, b0, more, &bar[1], uph, it);
+      else c_then_a<T, Q, 2, kTrace>(wp, ys, a_in, b0, more, &bar[1], uph, it);
     }
     ptx::fence_proxy_async();
+    hex_stamp<kTrace>(it, 7);
     __syncthreads();  // Ys complete (stage st), Us consumed (stage st + step), W holds t of st + step
     if (producer) {
       const std::int64_t e0 = st * NE;
@@ -835,6 +859,7 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
   auto kern = hex2_kernel<T, Q, NE2>;
   if constexpr (kMerged == 1) kern = hex5_kernel<T, Q, NE2, false>;
   if constexpr (kMerged == 2) kern = hex5_kernel<T, Q, NE2, true>;
+  if constexpr (kMerged == 3) kern = hex5_kernel<T, Q, NE2, true, true>;
   Hex2Dev d{};
   d.E = L.E;
   d.rows = R;
@@ -897,6 +922,7 @@ int launch_hex2_q(const HexLaunch& L, cudaStream_t st) {
     const bool merged_ok = L.rows == kMaxFields && L.E % 4 == 0 && L.ne != 2;
     if (merged_ok && L.variant == 5) return launch_hex2_t<double, Q, 4, 1>(L, st);
     if (merged_ok && L.variant == 2) return launch_hex2_t<double, Q, 4, 2>(L, st);
+    if (merged_ok && L.variant == 7) return launch_hex2_t<double, Q, 4, 3>(L, st);
     if (L.ne != 2 && L.E % 4 == 0) return launch_hex2_t<double, Q, 4>(L, st);
   }
   return launch_hex2_t<double, Q, 2>(L, st);
@@ -945,6 +971,12 @@ int launch_hex(const HexLaunch& L, void* stream) {
   if (grid > L.E / NE) grid = L.E / NE;
   hex_kernel<<<static_cast<int>(grid), kThreads, smem, static_cast<cudaStream_t>(stream)>>>(d);
   return cudaGetLastError();
+}
+
+// debug hook (tools/hex_trace.py): copies the v=7 instance's stamps to host
+extern "C" int fe_debug_hex_trace(void* host, size_t bytes) {
+  if (bytes > sizeof(g_hex_trace)) bytes = sizeof(g_hex_trace);
+  return cudaMemcpyFromSymbol(host, g_hex_trace, bytes);
 }
 
 // Creates the device's operator staging buffer and ordering event; called at

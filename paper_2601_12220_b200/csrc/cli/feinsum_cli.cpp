@@ -318,7 +318,7 @@ std::vector<std::string> default_candidates(const std::string& transform) {
   if (transform == "fem_grad/v1")
     return {"stages=4", "stages=4;te=16", "stages=3;ept=2", "stages=4;ept=2", "stages=3;ept=2;te=64"};
   if (transform == "gett_dmma/v1") return {"stages=2;group=6", "stages=2;group=12", "stages=3;group=12"};
-  if (transform == "hex_sumfact/v1") return {"", "ne=2", "v=1"};
+  if (transform == "hex_sumfact/v1") return {"", "v=3", "ne=2", "v=1"};
   if (transform == "tt/v1") return {"", "tc=1"};
   return {""};
 }

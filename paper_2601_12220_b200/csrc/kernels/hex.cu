@@ -653,7 +653,10 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex2_kernel(const
 // stores its partial before running A (nothing to wait for); directions 1 and
 // 2 run A first and then take their turn in the chain, so the chain's waits
 // are hidden behind A. Arithmetic and summation order are those of v2: the
-// output is bitwise identical.
+// output is bitwise identical. kChainEarly: directions below it take their
+// chain step right after C (default 2: x = 0 stores, x = 1 adds as soon as
+// x = 0 has stored, both then run A; x = 2 runs A first and adds last, so
+// the segment ends with one chain step instead of two serialised ones).
 // FE_HEX_TRACE instance (meta v=7): per-warp clock64 stamps of CTA 0 for the
 // first kTraceIters stages, read back by tools/hex_trace.py through
 // fe_debug_hex_trace (not part of the ABI). ptxas may move a clock read
@@ -689,23 +692,23 @@ __device__ __forceinline__ void chain_store(const T (&v)[Q][Q], T* ys, int b0) {
 }
 
 // one thread's merged segment: C(s) on its W plane, A(s+1) into the same plane
-template <typename T, int Q, int D, bool kTrace>
+template <typename T, int Q, int D, bool kTrace, int kChainEarly>
 __device__ __forceinline__ void c_then_a(T* w, T* ys, const T* a_in, int b0, bool next, std::uint64_t* ubar,
                                          std::uint32_t uphase, int it) {
   T v[Q][Q];
   sweep_c<T, Q, D>(w, v);
   hex_stamp<kTrace>(it, 4);
-  if constexpr (D == 0) chain_store<T, Q, 0>(v, ys, b0);
+  if constexpr (D < kChainEarly) chain_store<T, Q, D>(v, ys, b0);
   if (next) {
     ptx::mbar_wait(ubar, uphase);
     hex_stamp<kTrace>(it, 5);
     pass_a<T, Q, D>(a_in, w);
   }
   hex_stamp<kTrace>(it, 6);
-  if constexpr (D > 0) chain_store<T, Q, D>(v, ys, b0);
+  if constexpr (D >= kChainEarly) chain_store<T, Q, D>(v, ys, b0);
 }
 
-template <typename T, int Q, int NE2, bool kSplitB, bool kTrace = false>
+template <typename T, int Q, int NE2, bool kSplitB, bool kTrace = false, int kChainEarly = 1>
 __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex5_kernel(const __grid_constant__ Hex2Dev p) {
   constexpr int NE = NE2;
   constexpr int Q2 = Hx<Q>::Q2, Q3 = Hx<Q>::Q3, CS = Hx<Q>::CS;
@@ -815,9 +818,9 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex5_kernel(const
 
     if (pactive) {
       const std::uint32_t uph = static_cast<std::uint32_t>((it + 1) & 1);
-      if (dir == 0) c_then_a<T, Q, 0, kTrace>(wp, ys, a_in, b0, more, &bar[1], uph, it);
-      else if (dir == 1) c_then_a<T, Q, 1, kTrace>(wp, ys, a_in, b0, more, &bar[1], uph, it);
-      else c_then_a<T, Q, 2, kTrace>(wp, ys, a_in, b0, more, &bar[1], uph, it);
+      if (dir == 0) c_then_a<T, Q, 0, kTrace, kChainEarly>(wp, ys, a_in, b0, more, &bar[1], uph, it);
+      else if (dir == 1) c_then_a<T, Q, 1, kTrace, kChainEarly>(wp, ys, a_in, b0, more, &bar[1], uph, it);
+      else c_then_a<T, Q, 2, kTrace, kChainEarly>(wp, ys, a_in, b0, more, &bar[1], uph, it);
     }
     ptx::fence_proxy_async();
     hex_stamp<kTrace>(it, 7);
@@ -857,9 +860,10 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
   const int nblk = NE2 * R;
   constexpr int threads = HexCfg<Q, NE2>::kThreads;
   auto kern = hex2_kernel<T, Q, NE2>;
-  if constexpr (kMerged == 1) kern = hex5_kernel<T, Q, NE2, false>;
-  if constexpr (kMerged == 2) kern = hex5_kernel<T, Q, NE2, true>;
-  if constexpr (kMerged == 3) kern = hex5_kernel<T, Q, NE2, true, true>;
+  if constexpr (kMerged == 1) kern = hex5_kernel<T, Q, NE2, false, false, 1>;
+  if constexpr (kMerged == 2) kern = hex5_kernel<T, Q, NE2, true, false, 2>;
+  if constexpr (kMerged == 3) kern = hex5_kernel<T, Q, NE2, true, true, 2>;
+  if constexpr (kMerged == 4) kern = hex5_kernel<T, Q, NE2, true, false, 1>;
   Hex2Dev d{};
   d.E = L.E;
   d.rows = R;
@@ -918,11 +922,14 @@ int launch_hex2_q(const HexLaunch& L, cudaStream_t st) {
   if constexpr (Q < 6) {
     // v2 (default) takes the merged-stage kernel where it applies (eight
     // fields: one warp per (direction, plane) over 32 cubes); v3 forces the
-    // three-barrier kernel, v5 the merged one without the pass-B split
+    // three-barrier kernel; A/B variants of the merged one: v5 without the
+    // pass-B split and with only direction 0's chain step early, v6 with the
+    // split and only direction 0 early; v7 the default with FE_HEX_TRACE stamps
     const bool merged_ok = L.rows == kMaxFields && L.E % 4 == 0 && L.ne != 2;
     if (merged_ok && L.variant == 5) return launch_hex2_t<double, Q, 4, 1>(L, st);
     if (merged_ok && L.variant == 2) return launch_hex2_t<double, Q, 4, 2>(L, st);
     if (merged_ok && L.variant == 7) return launch_hex2_t<double, Q, 4, 3>(L, st);
+    if (merged_ok && L.variant == 6) return launch_hex2_t<double, Q, 4, 4>(L, st);
     if (L.ne != 2 && L.E % 4 == 0) return launch_hex2_t<double, Q, 4>(L, st);
   }
   return launch_hex2_t<double, Q, 2>(L, st);

@@ -42,6 +42,20 @@ def einsum_case(e, opts=None, tol=1e-12, seed=3):
     return plan.info["transform"] + " " + plan.info.get("meta", "")
 
 
+def hex_merged_case():
+    """The merged-stage hex kernel (eight fields) with two stages on the first
+    CTAs (E = 600: 150 four-element stages over the 148-CTA grid), so C(s) and
+    A(s+1) share a segment; bitwise against the three-barrier kernel (v=3),
+    which the parity suite pins to the reference."""
+    e = C.hex_poisson(E=600, b=8)
+    b = refpy.random_bindings(e, 7)
+    got = run(fe.Plan(einsum=e), b)
+    want = run(fe.Plan(einsum=e, options={"meta": "v=3", "transform": "hex_sumfact/v1"}), b)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+    return "hex_sumfact/v1 (merged, vs v=3)"
+
+
 def kernel_case(fk, rows, shape, opts=None, seed=5, post=None):
     import re
     arrays = []
@@ -85,6 +99,7 @@ CASES = {
     "tt_tc": lambda: einsum_case(C.tensor_train(n=4, r=64, dtype="float32"), {"meta": "tc=1"}, tol=1e-4),
     "hex2": lambda: einsum_case(C.hex_poisson(E=8, b=2)),
     "hex1": lambda: einsum_case(C.hex_poisson(E=8, b=2), {"meta": "v=1"}),
+    "hex5": lambda: hex_merged_case(),
     "path": lambda: einsum_case({"i_out": ["a", "d"], "i_in": [["a", "b"], ["b", "c"], ["c", "d"]],
                                  "args": [[{"name": n, "shape": [48, 48], "dtype": "float64"} for n in "ABC"]]}),
     "tab_vm": lambda: kernel_case(C.wave_kernel_nonlinear(E=512), 3, [3, 512, 10], {"codegen": False}),

@@ -374,14 +374,16 @@ def gpu_arm(args):
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["kernel"] = w.name + ":" + w.transform
         roof["traffic"] = None
-        try:  # dram bytes per launch of this config's kernel from the committed ncu capture
-            with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
-                tr = json.load(f)["per_config"].get(w.name.split("@")[0])
+        for rnd in ("r02", "r01"):  # dram bytes per launch of this config's kernel, newest committed ncu capture
+            try:
+                with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as f:
+                    tr = json.load(f)["per_config"].get(w.name.split("@")[0])
+            except (OSError, ValueError, KeyError):
+                continue
             if tr:
                 roof["traffic"] = tr["dram_bytes"]
-                roof["traffic_source"] = "profiles/r01/traffic.json (ncu --set full, %s)" % tr["kernel"]
-        except (OSError, ValueError, KeyError):
-            pass
+                roof["traffic_source"] = "profiles/%s/traffic.json (ncu --set full, %s)" % (rnd, tr["kernel"])
+                break
 
     extras = None
     if world == 1 and not args.no_extras:

@@ -111,8 +111,12 @@ int slot_of(std::vector<int>* slots, int leaf, int cap) {
 // register and exactly the VM's rounding. Operand parameter k is the local
 // p<k> (declared by the caller); `read` renders a leaf read as a double
 // expression ("" = unsupported). The value ends in r0. False if unsupported.
+// fast: exp / sin / cos as fastmath.cuh's range-unchecked straight-line forms,
+// each argument's range test and-ed into the caller's `fe_ok` (the caller
+// re-evaluates with the checked forms when it is false: same values where
+// the fast form applies, so the result never depends on the variant).
 bool emit_program(const Plan& p, const OperandStatic& op, const std::function<std::string(const VmRead&)>& read,
-                  const std::string& ind, std::ostringstream& s) {
+                  const std::string& ind, std::ostringstream& s, bool fast = false) {
   s << ind << "double r0 = 0.0";
   for (int r = 1; r < kMaxVmRegs; ++r) s << ", r" << r << " = 0.0";
   s << ";\n";
@@ -133,9 +137,18 @@ bool emit_program(const Plan& p, const OperandStatic& op, const std::function<st
       case VM_SUB: v = "__dsub_rn(" + a + ", " + b + ")"; break;
       case VM_MUL: v = "__dmul_rn(" + a + ", " + b + ")"; break;
       case VM_DIV: v = "__ddiv_rn(" + a + ", " + b + ")"; break;
-      case VM_SIN: v = "sin(" + a + ")"; break;
-      case VM_COS: v = "cos(" + a + ")"; break;
-      case VM_EXP: v = "exp(" + a + ")"; break;
+      case VM_SIN:
+      case VM_COS:
+      case VM_EXP: {
+        const char* fn = in.code == VM_SIN ? "sin" : in.code == VM_COS ? "cos" : "exp";
+        if (fast) {
+          s << ind << "fe_ok = fe_ok & feb200::fe_" << (in.code == VM_EXP ? "exp" : "trig") << "_ok(" << a << ");\n";
+          v = std::string("feb200::fe_") + fn + "_fast(" + a + ")";
+        } else {
+          v = std::string("feb200::fe_") + fn + "(" + a + ")";
+        }
+        break;
+      }
       case VM_RECIP: v = "__ddiv_rn(1.0, " + a + ")"; break;
       default: return false;  // sqrt: complex plans only
     }
@@ -162,7 +175,7 @@ void emit_decompose(const std::vector<std::int64_t>& shape, const std::string& t
 std::string tab_kernel_source(const Plan& p, const OperandStatic& op, const ArrayMeta& meta,
                               std::vector<int>* leaf_slots) {
   std::ostringstream s;
-  s << "struct TabArgs { const void* leaf[" << kTabLeaves << "]; double* out; long long count; };\n"
+  s << "#include \"fastmath.cuh\"\nstruct TabArgs { const void* leaf[" << kTabLeaves << "]; double* out; long long count; };\n"
     << "extern \"C\" __global__ void __launch_bounds__(256) fe_tab(const TabArgs a) {\n"
     << "  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < a.count;\n"
     << "       t += (long long)gridDim.x * blockDim.x) {\n";
@@ -186,7 +199,7 @@ std::string epi_kernel_source(const Plan& p, const OperandStatic& op, const Arra
   if (out_storage != ST_F64 && out_storage != ST_F32) return "";
   const std::string T = out_storage == ST_F64 ? "double" : "float";
   std::ostringstream s;
-  s << "struct TabArgs { const void* leaf[" << kTabLeaves << "]; double* out; long long count; };\n"
+  s << "#include \"fastmath.cuh\"\nstruct TabArgs { const void* leaf[" << kTabLeaves << "]; double* out; long long count; };\n"
     << "extern \"C\" __global__ void __launch_bounds__(256) fe_epi(const TabArgs a) {\n"
     << "  " << T << "* out = (" << T << "*)a.out;\n"
     << "  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < a.count;\n"
@@ -283,9 +296,12 @@ std::string fem_rtc_source(const Plan& p, int te, int ept, bool dsmem, std::vect
   // pass 2: prologue — every staged value of this (v) point is read into a
   // register first (the rows' programs then overlap), then each row's value
   std::ostringstream pro, epi;
+  std::vector<int> fast_rows;
+  std::vector<std::string> fast_body, slow_body;
   pro << "      const double* __restrict__ sd = (const double*)su;\n";
   for (size_t k = 0; k < staged.size(); ++k)
     pro << "      const double s" << k << " = sd[" << k << " * kUTile + v];\n";
+  pro << "@FASTBLOCK@";
   for (int q = 0; q < f.rows; ++q) {
     pro << "      {  // canonical row " << q << "\n";
     const auto& terms = f.u_terms[static_cast<size_t>(q)];
@@ -310,12 +326,28 @@ std::string fem_rtc_source(const Plan& p, int te, int ept, bool dsmem, std::vect
         if (stageable(rd, 0, 1)) return "s" + std::to_string(tile_index(q, rd.leaf));
         return aux_read(rd);
       };
-      std::ostringstream body;
-      if (!emit_program(p, op, read, "          ", body)) {
+      bool global_reads = false;
+      auto read_chk = [&](const VmRead& rd) -> std::string {
+        if (!stageable(rd, 0, 1)) global_reads = true;
+        return read(rd);
+      };
+      std::ostringstream body, fast;
+      if (!emit_program(p, op, read_chk, "          ", body)) {
         *why = "operand program of row " + std::to_string(q) + " not expressible";
         return "";
       }
-      pro << "        double val = 0.0;\n        if (live) {\n" << body.str() << "          val = r0;\n        }\n";
+      if (!global_reads && emit_program(p, op, read, "          ", fast, true)) {
+        // every read is a staged value (registers, valid for dead points
+        // too): this row joins the point's straight-line block of fast
+        // forms (emitted after the loop over rows), and only a point whose
+        // arguments leave their range re-runs the checked forms
+        fast_rows.push_back(q);
+        fast_body.push_back(fast.str());
+        slow_body.push_back(body.str());
+        pro << "        double val = live ? fv" << q << " : 0.0;\n";
+      } else {
+        pro << "        double val = 0.0;\n        if (live) {\n" << body.str() << "          val = r0;\n        }\n";
+      }
     }
     pro << "        uc[" << q << " * kUTile + v] = val;\n      }\n";
     // epilogue of the caller row this canonical row writes
@@ -334,9 +366,29 @@ std::string fem_rtc_source(const Plan& p, int te, int ept, bool dsmem, std::vect
       epi << "      case " << q << ": {\n" << body.str() << "        return r0;\n      }\n";
     }
   }
+  {
+    // the fast block: every fast row's program back to back (no branch
+    // between them, so their long dependency chains interleave), one range
+    // test for the point, the checked forms only when it fails
+    std::ostringstream fb;
+    if (!fast_rows.empty()) {
+      fb << "      bool fe_ok = true;\n      double";
+      for (size_t k = 0; k < fast_rows.size(); ++k) fb << (k ? ", fv" : " fv") << fast_rows[k];
+      fb << ";\n";
+      for (size_t k = 0; k < fast_rows.size(); ++k)
+        fb << "      {\n" << fast_body[k] << "        fv" << fast_rows[k] << " = r0;\n      }\n";
+      fb << "      if (!fe_ok) {\n";
+      for (size_t k = 0; k < fast_rows.size(); ++k)
+        fb << "        {\n" << slow_body[k] << "          fv" << fast_rows[k] << " = r0;\n        }\n";
+      fb << "      }\n";
+    }
+    std::string ps = pro.str();
+    ps.replace(ps.find("@FASTBLOCK@"), 11, fb.str());
+    pro.str(ps);
+  }
   const int consumers = (te * f.NI / ept + 31) / 32 * 32;
   std::ostringstream s;
-  s << "#include \"fem_grad.cuh\"\n"
+  s << "#include \"fastmath.cuh\"\n#include \"fem_grad.cuh\"\n"
     << "using namespace feb200;\nusing namespace feb200::fem;\n"
     << "struct GenPro {\n  static constexpr bool kPlain = false;\n  static constexpr bool kPipe = true;\n"
     << "  template <typename T, int kUTile, int kConsumers>\n"

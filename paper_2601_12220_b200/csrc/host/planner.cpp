@@ -1999,7 +1999,10 @@ std::unique_ptr<Plan> make_functional_plan(const BatchedEinsum& skeleton,
 
 namespace {
 void execute_on(const Plan& plan, const void* const* d_in, void* const* d_out, void* stream, bool* epi_done);
-std::mutex g_scratch_mu[16];
+// recursive: a path plan's execute holds its bucket while it executes its
+// step plans, whose addresses can hash to the same bucket (a plain mutex
+// self-deadlocked there, intermittently: 1 in 16 per step)
+std::recursive_mutex g_scratch_mu[16];
 
 // the rows' epilogues as in-place passes over the outputs (families that do
 // not fuse them)
@@ -2028,7 +2031,7 @@ void execute(const Plan& plan, const void* const* d_in, void* const* d_out, void
     if (!epi_done) run_epilogues(plan, d_in, d_out, stream);
     return;
   }
-  std::lock_guard<std::mutex> lock(g_scratch_mu[(reinterpret_cast<std::uintptr_t>(&plan) >> 6) & 15]);
+  std::lock_guard<std::recursive_mutex> lock(g_scratch_mu[(reinterpret_cast<std::uintptr_t>(&plan) >> 6) & 15]);
   auto st = static_cast<cudaStream_t>(stream);
   cuda_check(cudaStreamWaitEvent(st, plan.last_use, 0), "plan scratch ordering");
   execute_on(plan, d_in, d_out, stream, &epi_done);

@@ -11,6 +11,7 @@
 #include <cuda_fp16.h>
 #include <cstdint>
 
+#include "fastmath.cuh"
 #include "launch.h"
 
 namespace feb200 {
@@ -43,18 +44,20 @@ __device__ __forceinline__ cdbl cdiv(cdbl x, cdbl y) {
   return cdbl{__ddiv_rn(__dadd_rn(a, __dmul_rn(b, r)), den), __ddiv_rn(__dsub_rn(b, __dmul_rn(a, r)), den)};
 }
 
+// the real-argument functions are fastmath.cuh's (shared with the generated
+// programs so the VM and codegen agree bit for bit)
 __device__ __forceinline__ cdbl csin_(cdbl z) {
-  if (z.im == 0.0) return cdbl{sin(z.re), 0.0};
-  return cdbl{sin(z.re) * cosh(z.im), cos(z.re) * sinh(z.im)};
+  if (z.im == 0.0) return cdbl{fe_sin(z.re), 0.0};
+  return cdbl{fe_sin(z.re) * cosh(z.im), fe_cos(z.re) * sinh(z.im)};
 }
 __device__ __forceinline__ cdbl ccos_(cdbl z) {
-  if (z.im == 0.0) return cdbl{cos(z.re), -0.0 * sin(z.re)};
-  return cdbl{cos(z.re) * cosh(z.im), -sin(z.re) * sinh(z.im)};
+  if (z.im == 0.0) return cdbl{fe_cos(z.re), -0.0 * fe_sin(z.re)};
+  return cdbl{fe_cos(z.re) * cosh(z.im), -fe_sin(z.re) * sinh(z.im)};
 }
 __device__ __forceinline__ cdbl cexp_(cdbl z) {
-  const double m = exp(z.re);
+  const double m = fe_exp(z.re);
   if (z.im == 0.0) return cdbl{m, 0.0};
-  return cdbl{m * cos(z.im), m * sin(z.im)};
+  return cdbl{m * fe_cos(z.im), m * fe_sin(z.im)};
 }
 // principal square root; sqrt(-4) = 2i as std::sqrt(std::complex) gives
 __device__ __forceinline__ cdbl csqrt_(cdbl z) {
@@ -209,9 +212,9 @@ __device__ inline double eval_vm_real(const OperandStatic& op, const OperandEnv&
       case VM_SUB: v = __dsub_rn(a, b); break;
       case VM_MUL: v = __dmul_rn(a, b); break;
       case VM_DIV: v = __ddiv_rn(a, b); break;
-      case VM_SIN: v = sin(a); break;
-      case VM_COS: v = cos(a); break;
-      case VM_EXP: v = exp(a); break;
+      case VM_SIN: v = fe_sin(a); break;
+      case VM_COS: v = fe_cos(a); break;
+      case VM_EXP: v = fe_exp(a); break;
       case VM_SQRT: v = sqrt(a); break;  // not reached: sqrt makes the plan complex
       case VM_RECIP: v = __ddiv_rn(1.0, a); break;
     }

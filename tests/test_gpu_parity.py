@@ -151,6 +151,23 @@ def test_contraction_path(fe, ref, torch_cuda):
             assert g.dtype == np.float32 and rel_err(g, w) <= 1e-5, k
 
 
+def test_path_plans_execute_many(fe, ref, torch_cuda):
+    """A path plan executes its step plans while holding its scratch lock;
+    with the lock a plain mutex hashed by plan address, a step plan that
+    hashed to the same bucket deadlocked (1 in 16 per step). 48 fresh
+    three-step plans make a collision near certain if the lock regressed."""
+    m = lambda n, s: {"name": n, "shape": s, "dtype": "float64"}  # noqa: E731
+    e = {"i_out": ["a", "d"], "i_in": [["a", "b"], ["b", "c"], ["c", "d"]],
+         "args": [[m("A", [48, 64]), m("B", [64, 72]), m("C", [72, 40])]]}
+    b = ref.random_bindings(e, 5)
+    want = [w.real for w in ref.evaluate(e, b)]
+    for _ in range(48):
+        plan = fe.Plan(einsum=e)
+        assert plan.info["transform"] == "path/v1"
+        for g, w in zip(run_plan(torch_cuda, plan, b), want):
+            assert rel_err(g, w) <= FP64_TOL
+
+
 def test_generic_complex_bit_exact(fe, ref, torch_cuda):
     rng = np.random.default_rng(0)
     for seed in range(20):

@@ -18,6 +18,21 @@
 
 namespace feb200 {
 
+// Polynomial coefficients in the constant bank: each DFMA then reads its
+// coefficient as a c[bank][offset] operand (double immediates do not exist:
+// as literals every coefficient cost two UMOVs per use, 19% of the fused C5
+// prologue's instructions)
+static __constant__ double kFeExp[14] = {
+    1.6059043836821614599e-10, 2.0876756987868098979e-09, 2.5052108385441718775e-08, 2.7557319223985890653e-07,
+    2.7557319223985892510e-06, 2.4801587301587301566e-05, 1.9841269841269841253e-04, 1.3888888888888889419e-03,
+    8.3333333333333332177e-03, 4.1666666666666664354e-02, 1.6666666666666665741e-01, 0.5, 1.0, 1.0};  // 1/k!, k = 13..0
+static __constant__ double kFeSin[6] = {1.58969099521155010221e-10, -2.50507602534068634195e-08,
+                                        2.75573137070700676789e-06, -1.98412698298579493134e-04,
+                                        8.33333333332248946124e-03, -1.66666666666666324348e-01};
+static __constant__ double kFeCos[6] = {-1.13596475577881948265e-11, 2.08757232129817482790e-09,
+                                        -2.75573143513906633035e-07, 2.48015872894767294178e-05,
+                                        -1.38888888888741095749e-03, 4.16666666666666019037e-02};
+
 __device__ __forceinline__ bool fe_exp_ok(double x) { return fabs(x) <= 700.0; }
 __device__ __forceinline__ bool fe_trig_ok(double x) { return fabs(x) <= 1.0e5; }
 
@@ -26,20 +41,9 @@ __device__ __forceinline__ double fe_exp_fast(double x) {
   double r = fma(-n, 6.93147180369123816490e-01, x);  // ln2_hi (fdlibm): n * ln2_hi exact
   r = fma(-n, 1.90821492927058770002e-10, r);        // ln2_lo
   // e^r, |r| <= 0.3466: sum_{k<=13} r^k / k!  (truncation < 5e-18 relative)
-  double p = 1.6059043836821614599e-10;              // 1/13!
-  p = fma(p, r, 2.0876756987868098979e-09);          // 1/12!
-  p = fma(p, r, 2.5052108385441718775e-08);          // 1/11!
-  p = fma(p, r, 2.7557319223985890653e-07);          // 1/10!
-  p = fma(p, r, 2.7557319223985892510e-06);          // 1/9!
-  p = fma(p, r, 2.4801587301587301566e-05);          // 1/8!
-  p = fma(p, r, 1.9841269841269841253e-04);          // 1/7!
-  p = fma(p, r, 1.3888888888888889419e-03);          // 1/6!
-  p = fma(p, r, 8.3333333333333332177e-03);          // 1/5!
-  p = fma(p, r, 4.1666666666666664354e-02);          // 1/4!
-  p = fma(p, r, 1.6666666666666665741e-01);          // 1/3!
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  double p = kFeExp[0];
+#pragma unroll
+  for (int k = 1; k < 14; ++k) p = fma(p, r, kFeExp[k]);
   // times 2^n: |n| <= 1010 and p in [0.70, 1.42], so the result stays normal
   const long long k = static_cast<long long>(n);
   return __longlong_as_double(__double_as_longlong(p) + (k << 52));
@@ -48,21 +52,15 @@ __device__ __forceinline__ double fe_exp_fast(double x) {
 // sin(r) and cos(r) on |r| <= pi/4 (fdlibm __kernel_sin / __kernel_cos
 // minimax coefficients, tail correction omitted: within ~2 ulp)
 __device__ __forceinline__ double fe_sin_kernel(double r, double s) {
-  double p = 1.58969099521155010221e-10;
-  p = fma(p, s, -2.50507602534068634195e-08);
-  p = fma(p, s, 2.75573137070700676789e-06);
-  p = fma(p, s, -1.98412698298579493134e-04);
-  p = fma(p, s, 8.33333333332248946124e-03);
-  p = fma(p, s, -1.66666666666666324348e-01);
+  double p = kFeSin[0];
+#pragma unroll
+  for (int k = 1; k < 6; ++k) p = fma(p, s, kFeSin[k]);
   return fma(r * s, p, r);
 }
 __device__ __forceinline__ double fe_cos_kernel(double s) {
-  double p = -1.13596475577881948265e-11;
-  p = fma(p, s, 2.08757232129817482790e-09);
-  p = fma(p, s, -2.75573143513906633035e-07);
-  p = fma(p, s, 2.48015872894767294178e-05);
-  p = fma(p, s, -1.38888888888741095749e-03);
-  p = fma(p, s, 4.16666666666666019037e-02);
+  double p = kFeCos[0];
+#pragma unroll
+  for (int k = 1; k < 6; ++k) p = fma(p, s, kFeCos[k]);
   return fma(s * s, p, fma(-0.5, s, 1.0));
 }
 

@@ -708,7 +708,7 @@ __device__ __forceinline__ void c_then_a(T* w, T* ys, const T* a_in, int b0, boo
   if constexpr (D >= kChainEarly) chain_store<T, Q, D>(v, ys, b0);
 }
 
-template <typename T, int Q, int NE2, bool kSplitB, bool kTrace = false, int kChainEarly = 1>
+template <typename T, int Q, int NE2, bool kSplitB, bool kTrace = false, int kChainEarly = 1, bool kPairFast = false>
 __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex5_kernel(const __grid_constant__ Hex2Dev p) {
   constexpr int NE = NE2;
   constexpr int Q2 = Hx<Q>::Q2, Q3 = Hx<Q>::Q3, CS = Hx<Q>::CS;
@@ -790,11 +790,26 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex5_kernel(const
     constexpr int nfull = kSplitB ? nbt / 128 * 128 : nbt;
     constexpr int nleft = nbt - nfull;
     static_assert(2 * nleft <= 32, "remainder fits one warp");
+    // task t -> (line kl, element el, first field f0): line fastest, or
+    // (kPairFast) field pair fastest, so the four lanes of one (element,
+    // line) read the same G words (broadcast) while W stays conflict free
+    // (pairs f0 = 0..3 sit NE * CS = 4 mod 16 doubles apart)
+    auto task = [&](int t, int& kl, int& el, int& f0) {
+      if constexpr (kPairFast) {
+        f0 = t % H;
+        kl = (t / H) % Q2;
+        el = t / (H * Q2);
+      } else {
+        kl = t % Q2;
+        const int r = t / Q2;
+        el = r % NE;
+        f0 = r / NE;
+      }
+    };
     if (threadIdx.x < nfull) {
-      const int t = threadIdx.x;
-      const int kl = t % Q2;
-      const int r = t / Q2;
-      const int el = r % NE, f0 = r / NE, f1 = f0 + H;
+      int kl, el, f0;
+      task(threadIdx.x, kl, el, f0);
+      const int f1 = f0 + H;
       const T* g = Gs + el * Q3 + kl;
       T* const wl[2] = {W + (f0 * NE + el) * CS + kl, W + (f1 * NE + el) * CS + kl};
       pass_b<T, Q, 2>(wl, ds, g, NE * Q3);
@@ -802,10 +817,9 @@ __global__ void __launch_bounds__(HexCfg<Q, NE2>::kThreads, 1) hex5_kernel(const
       // lanes 0-15 take the first field of the remainder pairs, 16-31 the
       // second: each half-warp walks consecutive lines (no bank conflicts)
       const int idx = threadIdx.x - nfull;
-      const int t = nfull + idx % nleft;
-      const int kl = t % Q2;
-      const int r = t / Q2;
-      const int el = r % NE, f = r / NE + (idx >= nleft ? H : 0);
+      int kl, el, f0;
+      task(nfull + idx % nleft, kl, el, f0);
+      const int f = f0 + (idx >= nleft ? H : 0);
       const T* g = Gs + el * Q3 + kl;
       T* const wl[1] = {W + (f * NE + el) * CS + kl};
       pass_b<T, Q, 1>(wl, ds, g, NE * Q3);
@@ -861,9 +875,10 @@ int launch_hex2_t(const HexLaunch& L, cudaStream_t st) {
   constexpr int threads = HexCfg<Q, NE2>::kThreads;
   auto kern = hex2_kernel<T, Q, NE2>;
   if constexpr (kMerged == 1) kern = hex5_kernel<T, Q, NE2, false, false, 1>;
-  if constexpr (kMerged == 2) kern = hex5_kernel<T, Q, NE2, true, false, 2>;
-  if constexpr (kMerged == 3) kern = hex5_kernel<T, Q, NE2, true, true, 2>;
+  if constexpr (kMerged == 2) kern = hex5_kernel<T, Q, NE2, true, false, 2, true>;
+  if constexpr (kMerged == 3) kern = hex5_kernel<T, Q, NE2, true, true, 2, true>;
   if constexpr (kMerged == 4) kern = hex5_kernel<T, Q, NE2, true, false, 1>;
+  if constexpr (kMerged == 5) kern = hex5_kernel<T, Q, NE2, true, false, 2, false>;
   Hex2Dev d{};
   d.E = L.E;
   d.rows = R;
@@ -924,12 +939,15 @@ int launch_hex2_q(const HexLaunch& L, cudaStream_t st) {
     // fields: one warp per (direction, plane) over 32 cubes); v3 forces the
     // three-barrier kernel; A/B variants of the merged one: v5 without the
     // pass-B split and with only direction 0's chain step early, v6 with the
-    // split and only direction 0 early; v7 the default with FE_HEX_TRACE stamps
+    // split and only direction 0 early (both: pass-B tasks line fastest), v9
+    // the default with line-fastest pass-B tasks; v7 the default with
+    // FE_HEX_TRACE stamps
     const bool merged_ok = L.rows == kMaxFields && L.E % 4 == 0 && L.ne != 2;
     if (merged_ok && L.variant == 5) return launch_hex2_t<double, Q, 4, 1>(L, st);
     if (merged_ok && L.variant == 2) return launch_hex2_t<double, Q, 4, 2>(L, st);
     if (merged_ok && L.variant == 7) return launch_hex2_t<double, Q, 4, 3>(L, st);
     if (merged_ok && L.variant == 6) return launch_hex2_t<double, Q, 4, 4>(L, st);
+    if (merged_ok && L.variant == 9) return launch_hex2_t<double, Q, 4, 5>(L, st);
     if (L.ne != 2 && L.E % 4 == 0) return launch_hex2_t<double, Q, 4>(L, st);
   }
   return launch_hex2_t<double, Q, 2>(L, st);

@@ -652,7 +652,7 @@ def test_tensor_train_f32_tensor_cores(fe, torch_cuda, n, meta):
 _HEX_WANT = {}
 
 
-@pytest.mark.parametrize("meta", ["", "ne=2", "v=1", "v=3", "v=5", "v=6", "v=7"])
+@pytest.mark.parametrize("meta", ["", "ne=2", "v=1", "v=3", "v=5", "v=6", "v=7", "v=9"])
 def test_hex_sumfact_small(fe, ref, torch_cuda, meta):
     """C2's sum-factorised operator at oracle-sized extents, every kernel
     variant (default: merged C/A stages with eight fields; v=3 the

@@ -56,8 +56,32 @@ struct HostPipe {
   }
 };
 
+// Row pipeline (fe_plan_execute_host on plans too small to chunk, with
+// several rows): each row runs as its own single-row plan, so row r's
+// outputs stream back while row r+1 computes and row r+2's private inputs
+// upload (C1: the 7.2 MB of outputs no longer wait for the whole batch).
+// Single-row plans do each element's arithmetic in the same order, so the
+// outputs are bitwise those of the batched execute.
+struct RowPipe {
+  std::vector<std::unique_ptr<feb200::Plan>> rows;
+  std::vector<std::vector<int>> src;   // row plan leaf -> plan leaf
+  std::vector<int> first_use;          // plan leaf -> first row that reads it
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  cudaEvent_t start = nullptr;
+  std::vector<cudaEvent_t> h2d_done, comp_done, d2h_done;
+  ~RowPipe() {
+    for (auto* v : {&h2d_done, &comp_done, &d2h_done})
+      for (cudaEvent_t e : *v) cudaEventDestroy(e);
+    if (start) cudaEventDestroy(start);
+    for (cudaStream_t q : {s_h2d, s_comp, s_d2h})
+      if (q) cudaStreamDestroy(q);
+  }
+};
+
 struct fe_plan_s {
   std::unique_ptr<feb200::Plan> plan;
+  std::unique_ptr<RowPipe> rowpipe;
+  bool rowpipe_tried = false;
   std::string options;  // creation options (sub-plans of the host pipeline reuse them)
   // staging buffers for fe_plan_execute_host, allocated on first use
   std::vector<void*> staged_in, staged_out;
@@ -616,6 +640,49 @@ void run_pipe(HostPipe& P, const void* const* h_in, void* const* h_out, cudaStre
 
 }  // namespace
 
+// Row pipeline of a plan, or nothing (one row, functional / complex / path
+// plans, or a row that does not plan on its own leaves)
+std::unique_ptr<RowPipe> make_rowpipe(const fe_plan_s& h) {
+  const feb200::Plan& p = *h.plan;
+  if (std::getenv("FE_NO_ROWPIPE") || p.skel.b() < 2 || p.functional || p.complex_mode || !p.tabs.empty() ||
+      p.family == feb200::Family::path || p.family == feb200::Family::generic)
+    return nullptr;
+  auto rp = std::make_unique<RowPipe>();
+  const feb200::PlanOptions opt = feb200::parse_options(h.options);
+  rp->first_use.assign(p.leaves.size(), -1);
+  try {
+    for (int r = 0; r < p.skel.b(); ++r) {
+      BatchedEinsum row;
+      row.i_in = p.skel.i_in;
+      row.i_out = p.skel.i_out;
+      row.args = {p.skel.args[static_cast<size_t>(r)]};
+      rp->rows.push_back(feb200::make_plan(row, opt));
+      const feb200::Plan& rpl = *rp->rows.back();
+      if (rpl.family != p.family || rpl.outputs[0].storage != p.outputs[static_cast<size_t>(r)].storage) return nullptr;
+      std::vector<int> src;
+      for (const auto& L : rpl.leaves) {
+        int k = -1;
+        for (size_t i = 0; i < p.leaves.size(); ++i)
+          if (p.leaves[i].meta.name == L.meta.name && p.leaves[i].storage == L.storage) k = static_cast<int>(i);
+        if (k < 0) return nullptr;
+        if (rp->first_use[static_cast<size_t>(k)] < 0) rp->first_use[static_cast<size_t>(k)] = r;
+        src.push_back(k);
+      }
+      rp->src.push_back(std::move(src));
+    }
+  } catch (const error&) {
+    return nullptr;
+  }
+  for (cudaStream_t* q : {&rp->s_h2d, &rp->s_comp, &rp->s_d2h})
+    cuda_ok(cudaStreamCreateWithFlags(q, cudaStreamNonBlocking), "stream");
+  cuda_ok(cudaEventCreateWithFlags(&rp->start, cudaEventDisableTiming), "event");
+  for (auto* v : {&rp->h2d_done, &rp->comp_done, &rp->d2h_done}) {
+    v->resize(rp->rows.size());
+    for (cudaEvent_t& e : *v) cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
+  return rp;
+}
+
 int fe_plan_execute_host(fe_plan_t plan, const void* const* h_in, void* const* h_out, void* stream) {
   return guarded([&] {
     const feb200::Plan& p = *plan->plan;
@@ -636,6 +703,37 @@ int fe_plan_execute_host(fe_plan_t plan, const void* const* h_in, void* const* h
       }
       return bufs[i];
     };
+    if (!plan->rowpipe_tried) {
+      plan->rowpipe_tried = true;
+      plan->rowpipe = make_rowpipe(*plan);
+    }
+    if (RowPipe* rp = plan->rowpipe.get()) {
+      // H2D of row r's not yet uploaded leaves | row r's kernels | row r's D2H
+      // on three streams; all device buffers are the plan's staging ones
+      cuda_ok(cudaEventRecord(rp->start, s), "event");
+      for (cudaStream_t q : {rp->s_h2d, rp->s_comp, rp->s_d2h}) cuda_ok(cudaStreamWaitEvent(q, rp->start, 0), "wait");
+      for (size_t r = 0; r < rp->rows.size(); ++r) {
+        for (size_t i = 0; i < p.leaves.size(); ++i)
+          if (rp->first_use[i] == static_cast<int>(r))
+            cuda_ok(cudaMemcpyAsync(ensure(plan->staged_in, i, p.leaves[i].bytes()), h_in[i],
+                                    static_cast<size_t>(p.leaves[i].bytes()), cudaMemcpyHostToDevice, rp->s_h2d),
+                    "H2D");
+        cuda_ok(cudaEventRecord(rp->h2d_done[r], rp->s_h2d), "event");
+        cuda_ok(cudaStreamWaitEvent(rp->s_comp, rp->h2d_done[r], 0), "wait");
+        std::vector<const void*> din;
+        for (int k : rp->src[r]) din.push_back(plan->staged_in[static_cast<size_t>(k)]);
+        void* dout = ensure(plan->staged_out, r, p.outputs[r].bytes());
+        feb200::execute(*rp->rows[r], din.data(), &dout, rp->s_comp);
+        cuda_ok(cudaEventRecord(rp->comp_done[r], rp->s_comp), "event");
+        cuda_ok(cudaStreamWaitEvent(rp->s_d2h, rp->comp_done[r], 0), "wait");
+        cuda_ok(cudaMemcpyAsync(h_out[r], dout, static_cast<size_t>(p.outputs[r].bytes()), cudaMemcpyDeviceToHost,
+                                rp->s_d2h),
+                "D2H");
+        cuda_ok(cudaEventRecord(rp->d2h_done[r], rp->s_d2h), "event");
+      }
+      cuda_ok(cudaStreamWaitEvent(s, rp->d2h_done.back(), 0), "wait");
+      return;
+    }
     std::vector<const void*> din;
     for (size_t i = 0; i < p.leaves.size(); ++i) {
       void* d = ensure(plan->staged_in, i, p.leaves[i].bytes());

@@ -717,15 +717,23 @@ def test_hex_sumfact_large_sampled(fe, torch_cuda):
         assert err <= FP64_TOL, q
 
 
-@pytest.mark.parametrize("name", ["C4-f64", "C2-small", "C3", "C1-f32-large", "hex-f32", "matmul-split", "path3"])
+@pytest.mark.parametrize("name", ["C4-f64", "C2-small", "C3", "C1-f32-large", "hex-f32", "matmul-split", "path3",
+                                  "C1-rows", "hex-rows"])
 def test_execute_host_pipelined(fe, torch_cuda, name):
     """fe_plan_execute_host on plans above the pipelining threshold runs the
     chunked H2D / kernels / D2H pipeline (sub-plans along the shard axis on
-    three streams); its results must equal the device-resident execute bitwise
-    (the chunks run the same kernels on independent slices)."""
+    three streams); smaller plans with several rows (C1-rows: the C1 config;
+    hex-rows: a small three-field hex) run the row pipeline (one single-row
+    plan per row, row r's D2H under row r+1's kernels). Either way the results
+    must equal the device-resident execute bitwise (the same per-element
+    arithmetic on independent slices / rows)."""
     from paper_2601_12220_b200 import configs as C
     torch = torch_cuda
-    if name == "C4-f64":
+    if name == "C1-rows":
+        plan = fe.Plan(einsum=C.fem_grad())
+    elif name == "hex-rows":
+        plan = fe.Plan(einsum=C.hex_poisson(E=4_000, b=3))
+    elif name == "C4-f64":
         plan = fe.Plan(einsum=C.tensor_train(n=4096))
     elif name == "C2-small":
         plan = fe.Plan(einsum=C.hex_poisson(E=40_000, b=3))

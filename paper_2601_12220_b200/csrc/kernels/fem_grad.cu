@@ -100,8 +100,15 @@ int launch_fem_grad_t(const FemGradLaunch& p, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-int launch_fem_grad_rtc(const FemGradLaunch& p, void* kernel, int te, int ept, void* stream) {
-  if (p.E == 0) return cudaSuccess;
+int launch_fem_grad_rtc(const FemGradLaunch& p_in, void* kernel, int te, int ept, void* stream) {
+  if (p_in.E == 0) return cudaSuccess;
+  // the generated instances run the pipelined prologue (three combined
+  // buffers): its rewrite of buffer k % 3 is ordered after every warp's reads
+  // of tile k - 3 only through the producer's full[k % S] wait, i.e. for
+  // S <= 3 stages (with four, a warp two tiles ahead overwrote a buffer a
+  // slow warp was still reading: compute-sanitizer racecheck, round 2)
+  FemGradLaunch p = p_in;
+  if (p.stages > 3) p.stages = 3;
   const int nj = p.NJ, ni = p.NI;
   const int threads = 32 + (te * ni / ept + 31) / 32 * 32;
   const size_t doubles = static_cast<size_t>(p.n_d) * p.NX * ni * nj +

@@ -252,7 +252,11 @@ __device__ __forceinline__ void fem_grad_body(const FemGradLaunch& p) {
   // named barrier, so warps drift up to one tile apart and one warp's
   // (latency-bound) operand programs overlap another's contraction and
   // stores. Three buffers: a warp writing tile it+1 can be one tile ahead
-  // of the slowest, which still reads tile it-1.
+  // of the slowest, which still reads tile it-1. Buffer (it+1) % 3 was last
+  // read for tile it-2; combine_tile(it+1) first waits on full[(it+1) % S],
+  // which the producer arms only after every warp released tile it+1-S — so
+  // the rewrite is ordered after those reads only for S <= 3 (the launch
+  // clamps the ring depth of pipelined instances to 3).
   auto combine_tile = [&](int k, std::int64_t tl) {
     const int sk = k % S;
     ptx::mbar_wait(&full[sk], static_cast<std::uint32_t>(k / S) & 1u);

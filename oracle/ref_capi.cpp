@@ -23,10 +23,10 @@
 #include "feinsum/notation.hpp"
 #include "feinsum/raising.hpp"
 #include "feinsum/rng.hpp"
-#include "einsum_json.hpp"
+#include "ref_json.hpp"
 
 using namespace feinsum;
-using fejson::Value;
+using oj::Value;
 
 namespace {
 
@@ -52,15 +52,15 @@ int guard(F&& f) {
   }
 }
 
-BatchedEinsum ein(const char* js) { return transport::einsum_from_json(fejson::parse(js)); }
+BatchedEinsum ein(const char* js) { return ot::einsum_from_json(oj::parse(js)); }
 
 Value canon_to_json(const CanonResult& c) {
   Value v = Value::obj();
-  v.set("canonical", transport::einsum_to_json(c.canonical));
-  v.set("sigma_idx", transport::strmap_to_json(c.sigma_idx));
-  v.set("sigma_arg", transport::strmap_to_json(c.sigma_arg));
-  v.set("sigma_row", transport::ints_to_json(c.sigma_row));
-  v.set("sigma_slot", transport::ints_to_json(c.sigma_slot));
+  v.set("canonical", ot::einsum_to_json(c.canonical));
+  v.set("sigma_idx", ot::strmap_to_json(c.sigma_idx));
+  v.set("sigma_arg", ot::strmap_to_json(c.sigma_arg));
+  v.set("sigma_row", ot::ints_to_json(c.sigma_row));
+  v.set("sigma_slot", ot::ints_to_json(c.sigma_slot));
   return v;
 }
 
@@ -92,7 +92,7 @@ ColoredDigraph graph_from_json(const Value& v) {
   return g;
 }
 
-void put(char** out, const Value& v) { *out = dup(fejson::dump(v)); }
+void put(char** out, const Value& v) { *out = dup(oj::dump(v)); }
 
 Bindings bind_universe(const BatchedEinsum& e, const double* const* in_c) {
   Bindings b;
@@ -122,7 +122,7 @@ const char* ref_last_error() { return g_err.c_str(); }
 void ref_free(char* p) { std::free(p); }
 
 int ref_parse_classic(const char* text, char** out) {
-  return guard([&] { put(out, transport::einsum_to_json(parse_classic(text))); });
+  return guard([&] { put(out, ot::einsum_to_json(parse_classic(text))); });
 }
 
 int ref_print_classic(const char* js, char** out) {
@@ -130,7 +130,7 @@ int ref_print_classic(const char* js, char** out) {
 }
 
 int ref_validate(const char* js, char** out) {
-  return guard([&] { put(out, transport::list_to_json(validate(ein(js)))); });
+  return guard([&] { put(out, ot::list_to_json(validate(ein(js)))); });
 }
 
 int ref_canonicalize(const char* js, char** out) {
@@ -149,7 +149,7 @@ int ref_canonical_key(const char* js, char** out) {
 int ref_generate_random(const char* params_js, std::uint64_t seed, char** out) {
   return guard([&] {
     GenParams p;
-    Value pv = fejson::parse(params_js);
+    Value pv = oj::parse(params_js);
     if (auto* x = pv.find("b_min")) p.b_min = static_cast<int>(x->as_int());
     if (auto* x = pv.find("b_max")) p.b_max = static_cast<int>(x->as_int());
     if (auto* x = pv.find("n_min")) p.n_min = static_cast<int>(x->as_int());
@@ -166,7 +166,7 @@ int ref_generate_random(const char* params_js, std::uint64_t seed, char** out) {
     }
     if (auto* x = pv.find("allow_empty_out")) p.allow_empty_out = x->b;
     if (auto* x = pv.find("allow_repeated_index")) p.allow_repeated_index = x->b;
-    put(out, transport::einsum_to_json(generate_random(p, seed)));
+    put(out, ot::einsum_to_json(generate_random(p, seed)));
   });
 }
 
@@ -174,8 +174,8 @@ int ref_scramble(const char* js, std::uint64_t seed, char** out) {
   return guard([&] {
     Scrambled s = scramble(ein(js), seed);
     Value v = Value::obj();
-    v.set("e", transport::einsum_to_json(s.e));
-    v.set("w", transport::witness_to_json(s.w));
+    v.set("e", ot::einsum_to_json(s.e));
+    v.set("w", ot::witness_to_json(s.w));
     put(out, v);
   });
 }
@@ -183,14 +183,14 @@ int ref_scramble(const char* js, std::uint64_t seed, char** out) {
 int ref_is_isomorphic(const char* a, const char* b, char** out) {
   return guard([&] {
     auto w = is_isomorphic(ein(a), ein(b));
-    put(out, w ? transport::witness_to_json(*w) : Value{});
+    put(out, w ? ot::witness_to_json(*w) : Value{});
   });
 }
 
 int ref_brute_force_isomorphic(const char* a, const char* b, std::uint64_t budget, char** out) {
   return guard([&] {
     auto w = brute_force_isomorphic(ein(a), ein(b), budget);
-    put(out, w ? transport::witness_to_json(*w) : Value{});
+    put(out, w ? ot::witness_to_json(*w) : Value{});
   });
 }
 
@@ -198,10 +198,10 @@ int ref_verify_witness(const char* a, const char* b, const char* w, char** out) 
   return guard([&] {
     std::vector<std::string> why;
     bool ok = verify_witness(ein(a), ein(b),
-                             transport::witness_from_json<SubstitutionWitness>(fejson::parse(w)), &why);
+                             ot::witness_from_json<SubstitutionWitness>(oj::parse(w)), &why);
     Value v = Value::obj();
     v.set("ok", Value::boolean_(ok));
-    v.set("why", transport::list_to_json(why));
+    v.set("why", ot::list_to_json(why));
     put(out, v);
   });
 }
@@ -232,14 +232,14 @@ int ref_induced_graph(const char* js, std::int64_t shuffle_seed, char** out) {
 
 int ref_canonical_labeling(const char* graph_js, char** out) {
   return guard([&] {
-    Relabeling r = canonical_labeling(graph_from_json(fejson::parse(graph_js)));
-    put(out, transport::ints_to_json(r.perm));
+    Relabeling r = canonical_labeling(graph_from_json(oj::parse(graph_js)));
+    put(out, ot::ints_to_json(r.perm));
   });
 }
 
 int ref_check_compliance(const char* graph_js, char** out) {
   return guard([&] {
-    put(out, transport::list_to_json(check_compliance(graph_from_json(fejson::parse(graph_js)))));
+    put(out, ot::list_to_json(check_compliance(graph_from_json(oj::parse(graph_js)))));
   });
 }
 
@@ -274,9 +274,9 @@ int ref_raise(const char* fk, char** out) {
     FunctionalKernel k = parse_kernel(fk);
     RaiseResult rr = raise_to_batched_einsum(k);
     Value v = Value::obj();
-    v.set("skeleton", transport::einsum_to_json(rr.f.skeleton));
-    v.set("sigma_arg", transport::strmap_to_json(rr.sigma_arg));
-    v.set("sigma_idx", transport::strmap_to_json(rr.sigma_idx));
+    v.set("skeleton", ot::einsum_to_json(rr.f.skeleton));
+    v.set("sigma_arg", ot::strmap_to_json(rr.sigma_arg));
+    v.set("sigma_idx", ot::strmap_to_json(rr.sigma_idx));
     Value fps = Value::obj();
     for (const auto& [name, op] : rr.f.operand_map) fps.set(name, Value::str(fingerprint(op)));
     v.set("fingerprints", std::move(fps));
@@ -290,10 +290,10 @@ int ref_identify(const char* fk, const char* js, char** out) {
   return guard([&] {
     MatchResult m = identify_as_einsum(parse_kernel(fk), ein(js));
     Value v = Value::obj();
-    v.set("sigma_idx", transport::strmap_to_json(m.sigma_idx));
-    v.set("sigma_arg", transport::strmap_to_json(m.sigma_arg));
-    v.set("sigma_arg_skeleton", transport::strmap_to_json(m.sigma_arg_skeleton));
-    v.set("sigma_row", transport::ints_to_json(m.sigma_row));
+    v.set("sigma_idx", ot::strmap_to_json(m.sigma_idx));
+    v.set("sigma_arg", ot::strmap_to_json(m.sigma_arg));
+    v.set("sigma_arg_skeleton", ot::strmap_to_json(m.sigma_arg_skeleton));
+    v.set("sigma_row", ot::ints_to_json(m.sigma_row));
     put(out, v);
   });
 }
@@ -320,7 +320,7 @@ int ref_cost(const char* js, char** out) {
 int ref_record_facts(const char* path, const char* facts_js) {
   return guard([&] {
     std::vector<FactRecord> batch;
-    for (const auto& f : fejson::parse(facts_js).a) {
+    for (const auto& f : oj::parse(facts_js).a) {
       FactRecord r;
       r.canonical_key = f.at("canonical_key").as_str();
       r.device_id = f.at("device_id").as_str();

@@ -202,6 +202,49 @@ def test_c5_nonlinear_fused_prologue(fe, ref, torch_cuda):
 
 
 @pytest.mark.gpu
+def test_c5_nonlinear_fastmath_ranges(fe, ref, torch_cuda):
+    """Arguments outside fastmath.cuh's straight-line ranges (|k| up to 3e6
+    for sin: beyond 1e5; |u| up to 720 for exp: beyond 700, overflow to inf
+    included) take the checked forms: the fused prologue (one range test per
+    point, the whole point re-run) and the device VM tables agree bitwise,
+    and both match the reference's libm within the fp64 bar."""
+    from paper_2601_12220_b200 import configs as C
+    E = 2_000
+    fk = C.wave_kernel_nonlinear(E=E)
+    arrays, b = bindings_for(ref, fk, 17)
+    rng = np.random.default_rng(5)
+    for q in (1, 2, 3):
+        k = np.asarray(b[f"k{q}"], dtype=np.float64)
+        u = np.asarray(b[f"u{q}"], dtype=np.float64)
+        big = rng.random(k.shape) < 0.05  # a few points per tile out of range
+        k = np.where(big, rng.uniform(-3e6, 3e6, k.shape), k)
+        u = np.where(rng.random(u.shape) < 0.05, rng.uniform(-720, 720, u.shape) / 40.0, u)
+        u = np.where(rng.random(u.shape) < 0.01, np.sign(u) * 710.0, u)
+        b[f"k{q}"], b[f"u{q}"] = k, u
+    plan = fe.Plan(kernel=fk)
+    assert plan.info["fem_codegen"] == "nvrtc"
+    got = run_plan(torch_cuda, plan, b)
+    vm = fe.Plan(kernel=fk, options={"codegen": False})
+    for g, v in zip(got, run_plan(torch_cuda, vm, b)):
+        assert np.array_equal(g, v)
+    want = ref.eval_kernel(fk, arrays, b, 3, [3, E, 10])
+    # |u| = 710 makes u^2 ~ 5e5 while the outputs stay O(10): the error of
+    # any summation order is relative to the terms' magnitude, so the bar is
+    # 1e-12 of the forward-error scale sum_{x,j} |J||D||s| (s from numpy)
+    J = np.abs(np.asarray(b["J"], dtype=np.float64).reshape(3, 3, E))
+    D = np.abs(np.asarray(b["D"], dtype=np.float64).reshape(3, 10, 10))
+    for q, (g, w) in enumerate(zip(got, want), start=1):
+        w = np.real(np.asarray(w)).reshape(g.shape)
+        u, k = (np.asarray(b[n], dtype=np.float64).reshape(E, 10) for n in (f"u{q}", f"k{q}"))
+        with np.errstate(over="ignore"):
+            sv = np.abs(u * u - np.sin(k) / (2.0 + np.exp(u)))
+        scale = np.einsum("xre,xij,ej->rei", J, D, sv)
+        fin = np.isfinite(w)
+        assert np.array_equal(np.isfinite(g), fin)
+        assert np.max(np.abs(g[fin] - w[fin]) / np.maximum(1.0, scale[fin])) <= FP64_TOL
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("E", [2_000, 2_046, 64 * 37 + 2])
 def test_c5_nonlinear_epilogue_fused(fe, ref, torch_cuda, E):
     """Epilogues fused into the fem_grad stores (ragged last tile included)."""

@@ -114,7 +114,11 @@ int fe_plan_execute(fe_plan_t plan, const void* const* d_in, void* const* d_out,
  * synchronized). Plans above 64 MB run as a pipeline of chunks (8; GETT: by wave fill) along the
  * shard axis: chunk k's H2D, chunk k-1's kernels and chunk k-2's D2H overlap
  * on internal streams (host buffers should be pinned for the copies to
- * overlap); `stream` resumes after the last D2H. */
+ * overlap); smaller plans with several rows (plain real operands) run one
+ * single-row plan per row so row r's D2H overlaps row r+1's kernels; either
+ * way the outputs equal fe_plan_execute's bitwise and `stream` resumes after
+ * the last D2H. Not for concurrent calls on one plan (the staging buffers and
+ * pipelines are the plan's). */
 int fe_plan_execute_host(fe_plan_t plan, const void* const* h_in, void* const* h_out, void* stream);
 /* tabulate one skeleton operand (materialize, raising.hpp:43) into
  * interleaved complex doubles */

@@ -310,10 +310,22 @@ def gpu_arm(args):
     if world > 1:
         dist.barrier()
 
-    mean_t = torch.tensor([sum(t) / len(t) for t in times], dtype=torch.float64, device=cdev)
+    # per config: the median of the K timed steps (each its own CUDA-event
+    # pair on the launch stream, L2 flushed before it). The mean is reported
+    # beside it: a multi-launch config occasionally waits for its host thread
+    # between launches while nvidia-smi samples the clocks (the sampler must
+    # run during the timed region), and one such step moved C5's mean by 40%.
+    def median(v):
+        v = sorted(v)
+        n = len(v)
+        return v[n // 2] if n % 2 else 0.5 * (v[n // 2 - 1] + v[n // 2])
+    mean_t = torch.tensor([median(t) for t in times], dtype=torch.float64, device=cdev)
+    avg_t = torch.tensor([sum(t) / len(t) for t in times], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(mean_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(avg_t, op=dist.ReduceOp.MAX)
     mean_t = mean_t.cpu().tolist()
+    avg_t = avg_t.cpu().tolist()
 
     peaks, peak_src = measured_peaks()
     fp64 = {}
@@ -338,7 +350,7 @@ def gpu_arm(args):
 
     per = {}
     rates = []
-    for w, t in zip(loads, mean_t):
+    for w, t, ta in zip(loads, mean_t, avg_t):
         agg_flops = w.global_flops  # the global (world x config) problem, one shard per rank
         gflops = agg_flops / t / 1e9
         rates.append(gflops)
@@ -346,7 +358,7 @@ def gpu_arm(args):
         # peak for the DMMA kernels, DFMA peak for the DFMA kernels)
         fp_peak = pipe_peak(w.pipe)[0] * 1e12
         roof_t = max(w.bytes / (peaks["hbm_gbs"] * 1e9), w.flops / fp_peak if fp_peak else 0.0)
-        per[w.name] = {"ms": t * 1e3, "gflops": gflops, "gbs": w.full.info["bytes"] / t / 1e9,
+        per[w.name] = {"ms": t * 1e3, "ms_mean": ta * 1e3, "gflops": gflops, "gbs": w.full.info["bytes"] / t / 1e9,
                        "transform": w.transform, "source": w.source, "flops": w.flops, "bytes": w.bytes,
                        "roof_ms": roof_t * 1e3, "roof_frac": roof_t / t,
                        "pipe": w.pipe,
@@ -409,6 +421,8 @@ def gpu_arm(args):
                        "suite": {n: CONFIG_DOC[n] for n in names}, "per_config": per, "skipped": skipped,
                        "l2": "flushed before every config launch: 256 MiB write, then the same 256 MiB read back (L2 cold for the inputs and clean)",
                        "parallelism": f"dp{world} (element/batch-axis shards, no collective; {args.scaling} scaling)",
+                       "statistic": "per config: median of the K timed steps (CUDA events; ms_mean beside it); "
+                                    "ms_per_step = sum of the per-config medians",
                        "wall_s_timed_region": wall},
             "roofline": roof, "fp64_peak_tflops": fp64, "clocks": clocks.summary(),
             "gpu_launches": args.steps * sum(w.launches for w in loads),

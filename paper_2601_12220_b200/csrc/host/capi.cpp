@@ -598,8 +598,34 @@ std::unique_ptr<HostPipe> make_pipe(const fe_plan_s& h) {
   return pipe;
 }
 
+// FE_PIPE_TRACE=1: timing events per pipeline step, printed to stderr after
+// the call (debug aid; synchronises)
+struct PipeTrace {
+  bool on = std::getenv("FE_PIPE_TRACE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  void mark(const std::string& what, cudaStream_t q) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, q);
+    ev.emplace_back(what, e);
+  }
+  ~PipeTrace() {
+    if (!on || ev.empty()) return;
+    for (auto& [what, e] : ev) {
+      cudaEventSynchronize(e);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev.front().second, e);
+      std::fprintf(stderr, "pipe %-16s %8.3f ms\n", what.c_str(), ms);
+    }
+    for (auto& kv : ev) cudaEventDestroy(kv.second);
+  }
+};
+
 void run_pipe(HostPipe& P, const void* const* h_in, void* const* h_out, cudaStream_t s) {
   const int chunks = static_cast<int>(P.parts.size());
+  PipeTrace tr;
+  tr.mark("start", s);
   cuda_ok(cudaEventRecord(P.start, s), "event");
   for (cudaStream_t q : {P.s_h2d, P.s_comp, P.s_d2h}) cuda_ok(cudaStreamWaitEvent(q, P.start, 0), "wait");
   // replicated inputs once per call
@@ -608,6 +634,7 @@ void run_pipe(HostPipe& P, const void* const* h_in, void* const* h_out, cudaStre
       cuda_ok(cudaMemcpyAsync(P.rep_in[i], h_in[i], static_cast<size_t>(P.parts[0]->leaves[i].bytes()),
                               cudaMemcpyHostToDevice, P.s_h2d),
               "H2D");
+  tr.mark("replicated h2d", P.s_h2d);
   for (int k = 0; k < chunks; ++k) {
     const int b = k & 1;
     // H2D of chunk k into slot b, once chunk k-2's kernels have read it
@@ -622,16 +649,19 @@ void run_pipe(HostPipe& P, const void* const* h_in, void* const* h_out, cudaStre
       din[i] = P.slot_in[b][i];
     }
     cuda_ok(cudaEventRecord(P.h2d_done[b], P.s_h2d), "event");
+    tr.mark("h2d " + std::to_string(k), P.s_h2d);
     // kernels of chunk k, once its inputs landed and chunk k-2's outputs left
     cuda_ok(cudaStreamWaitEvent(P.s_comp, P.h2d_done[b], 0), "wait");
     if (k >= 2) cuda_ok(cudaStreamWaitEvent(P.s_comp, P.d2h_done[b], 0), "wait");
     feb200::execute(*P.parts[k], din.data(), P.slot_out[b].data(), P.s_comp);
     cuda_ok(cudaEventRecord(P.comp_done[b], P.s_comp), "event");
+    tr.mark("comp " + std::to_string(k), P.s_comp);
     // D2H of chunk k's outputs
     cuda_ok(cudaStreamWaitEvent(P.s_d2h, P.comp_done[b], 0), "wait");
     for (size_t r = 0; r < P.out_slice.size(); ++r)
       copy_slice(P.out_slice[r], P.lo[k], P.hi[k], P.slot_out[b][r], h_out[r], false, P.s_d2h);
     cuda_ok(cudaEventRecord(P.d2h_done[b], P.s_d2h), "event");
+    tr.mark("d2h " + std::to_string(k), P.s_d2h);
   }
   // the caller's stream resumes after the last D2H (and with it everything)
   cuda_ok(cudaStreamWaitEvent(s, P.d2h_done[(chunks - 1) & 1], 0), "wait");

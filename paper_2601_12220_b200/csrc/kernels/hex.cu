@@ -9,10 +9,14 @@
 //   q_x = sum_y G[x,y] . t_y              pointwise 3x3 geometric factors
 //   y  += (B1[x] x B2[x] x B3[x])^T q_x   three transposed sweeps per x
 //
-// Two kernels. v1 (hex_kernel, meta v=1): register-plane passes with the 5x5
-// operators loaded from shared memory. v2 (hex2_kernel, the default, see the
-// comment above it): operators in the constant bank, pass ownership matched
-// to the sweeps (planes / lines / planes), four elements per stage.
+// Three kernels. v1 (hex_kernel, meta v=1): register-plane passes with the
+// 5x5 operators loaded from shared memory. hex2_kernel (meta v=3, and the
+// default below eight fields, see the comment above it): operators in the
+// constant bank, pass ownership matched to the sweeps (planes / lines /
+// planes), four elements per stage, three CTA barriers per stage. hex5_kernel
+// (the default for eight fields, C2): hex2 with pass C of stage s and pass A
+// of stage s+1 merged into one barrier-free segment (two barriers per stage),
+// pass-B tasks field pair fastest; bitwise equal to hex2.
 //
 // Common to both: persistent CTAs walk element stages (2 or 4 elements = one
 // contiguous bulk-copy run per array); one thread streams the stage's 9 G
